@@ -1,0 +1,196 @@
+// Layer-by-layer depthwise convolution (fcm_dw; the paper's LBL DW kernel) and the
+// offline PW weight packing kernel.
+//
+// NHWC path: one CTA per (output tile th x tw, 128-byte channel group). The input halo tile
+// ((th-1)s+k) x ((tw-1)s+k) x 128 B is staged in shared memory by ONE TMA load whose
+// out-of-bounds fill provides the zero padding (overlapping halos are re-loaded per
+// tile -- on B200 they are L2 hits). Lane = one 32-bit word of channels (conflict-free smem
+// reads); warps own output columns and slide a k x k register window down them, so each
+// staged word is read once per column. Output stores are 128 B per warp instruction.
+#include "common.cuh"
+#include "host.h"
+
+namespace fcm {
+
+template <int DT, int K, int S>
+__global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CUtensorMap tmx,
+                                                      const typename Tr<DT>::T* __restrict__ wdw, Epi ep,
+                                                      typename Tr<DT>::T* __restrict__ y, int C, int Ho, int Wo,
+                                                      int pt, int pl, int th, int tw, int tiles_x, int tiles_y) {
+  constexpr int V = Tr<DT>::VEC;
+  constexpr int KC = 32 * V;  // channels per 128-byte group
+  extern __shared__ __align__(128) uint32_t xs[];
+  __shared__ uint64_t bar;
+  const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
+  int t = blockIdx.x;
+  const int tx = t % tiles_x;
+  t /= tiles_x;
+  const int ty = t % tiles_y;
+  const int n = t / tiles_y;
+  const int c0 = blockIdx.y * KC;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmx);
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar, th_in * tw_in * 128);
+    tma_load_4d(xs, &tmx, &bar, c0, tx * tw * S - pl, ty * th * S - pt, n);
+  }
+  const int c = c0 + lane * V;
+  DwW<DT, K> W;
+  load_dw_weights<DT, K>(W, wdw, C, c);
+  EpiC ec[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ep, c + v, c + v < C);
+  mbar_wait(&bar, 0);
+  const int y0 = ty * th, x0 = tx * tw;
+  const int nrows = min(th, Ho - y0);
+  uint32_t* yw = reinterpret_cast<uint32_t*>(y);
+  for (int col = warp; col < tw; col += 4) {
+    const int x = x0 + col;
+    if (x >= Wo) break;
+    const uint32_t* src = xs + (col * S) * 32 + lane;
+    dw_column<DT, K, S>(src, 32, tw_in * 32, nrows, W, [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
+      if (c < C) {
+        const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
+        yw[(pix * C + c) / V] = epi_pack<DT>(acc, ec, ep);
+      }
+    });
+  }
+}
+
+// NCHW: plane-per-(n,c) direct convolution through the read-only cache (layout accepted for
+// completeness; the fused paths are NHWC).
+template <int DT>
+__global__ void dw_nchw_kernel(const typename Tr<DT>::T* __restrict__ x, const typename Tr<DT>::T* __restrict__ wdw,
+                               Epi ep, typename Tr<DT>::T* __restrict__ y, int C, int H, int W, int Ho, int Wo, int k,
+                               int s, int pt, int pl, long long total) {
+  using TT = typename Tr<DT>::T;
+  using A = typename Tr<DT>::acc_t;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int xo = idx % Wo;
+    long long r = idx / Wo;
+    const int yo = r % Ho;
+    r /= Ho;
+    const int c = r % C;
+    const long long plane = r;  // n*C + c
+    A acc = 0;
+    for (int i = 0; i < k; ++i) {
+      const int yi = yo * s - pt + i;
+      if (yi < 0 || yi >= H) continue;
+      for (int j = 0; j < k; ++j) {
+        const int xi = xo * s - pl + j;
+        if (xi < 0 || xi >= W) continue;
+        TT xv = x[(plane * H + yi) * W + xi];
+        TT wv = wdw[(i * k + j) * C + c];
+        if constexpr (DT == FCM_S8) acc += static_cast<int32_t>(xv) * static_cast<int32_t>(wv);
+        else if constexpr (DT == FCM_F32) acc = fmaf(xv, wv, acc);
+        else if constexpr (DT == FCM_BF16) acc = fmaf(__bfloat162float(xv), __bfloat162float(wv), acc);
+        else acc = fmaf(__half2float(xv), __half2float(wv), acc);
+      }
+    }
+    EpiC e = load_epi<DT>(ep, c, true);
+    if constexpr (DT == FCM_S8) y[idx] = static_cast<int8_t>(requant_i8(acc, e, ep.zp_out, ep.qmin, ep.qmax));
+    else if constexpr (DT == FCM_F32) y[idx] = epi_f(acc, e.sc, e.bi, ep.act);
+    else if constexpr (DT == FCM_BF16) y[idx] = __float2bfloat16_rn(epi_f(acc, e.sc, e.bi, ep.act));
+    else y[idx] = __float2half_rn(epi_f(acc, e.sc, e.bi, ep.act));
+  }
+}
+
+// Offline PW packing: canonical [C_in][C_out] -> K-major [C_out][C_in].
+template <typename TT>
+__global__ void pack_pw_kernel(const TT* __restrict__ w, TT* __restrict__ p, int cin, int cout) {
+  __shared__ TT tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx over cout, by over cin
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int ci = by + i, co = bx + threadIdx.x;
+    if (ci < cin && co < cout) tile[i][threadIdx.x] = w[(size_t)ci * cout + co];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int co = bx + i, ci = by + threadIdx.x;
+    if (ci < cin && co < cout) p[(size_t)co * cin + ci] = tile[threadIdx.x][i];
+  }
+}
+
+// ------------------------------------------------------------------------------- launchers
+template <int DT, int K, int S>
+static int launch_dw_t(const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  constexpr int ES = Tr<DT>::ES;
+  constexpr int KC = 128 / ES;
+  const int th = g.th, tw = g.tw;
+  const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
+  if (th_in > 256 || tw_in > 256) return set_error(FCM_E_INFEASIBLE, "dw tile halo exceeds the TMA box limit (256)");
+  CUtensorMap tm;
+  const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
+  const uint64_t strides[3] = {(uint64_t)g.C * ES, (uint64_t)g.W * g.C * ES, (uint64_t)g.H * g.W * g.C * ES};
+  const uint32_t box[4] = {(uint32_t)KC, (uint32_t)tw_in, (uint32_t)th_in, 1};
+  if (!encode_tmap(&tm, tmap_dtype(DT), 4, x, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return set_error(FCM_E_CUDA, "cuTensorMapEncodeTiled failed for the DW input");
+  const int tiles_x = (g.Wo + tw - 1) / tw, tiles_y = (g.Ho + th - 1) / th;
+  const size_t smem = (size_t)th_in * tw_in * 128;
+  if (smem > (size_t)device_props().smem_optin) return set_error(FCM_E_INFEASIBLE, "dw tile exceeds shared memory");
+  auto kern = dw_nhwc_kernel<DT, K, S>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(tiles_x * tiles_y * g.N, (g.C + KC - 1) / KC);
+  using TT = typename Tr<DT>::T;
+  kern<<<grid, 128, smem, st>>>(tm, static_cast<const TT*>(wdw), ep, static_cast<TT*>(y), g.C, g.Ho, g.Wo, g.pt, g.pl,
+                                th, tw, tiles_x, tiles_y);
+  return check_launch("dw_nhwc_kernel");
+}
+
+template <int DT>
+static int launch_dw_dt(const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  if (g.k == 3 && g.s == 1) return launch_dw_t<DT, 3, 1>(x, wdw, ep, y, g, st);
+  if (g.k == 3 && g.s == 2) return launch_dw_t<DT, 3, 2>(x, wdw, ep, y, g, st);
+  if (g.k == 5 && g.s == 1) return launch_dw_t<DT, 5, 1>(x, wdw, ep, y, g, st);
+  if (g.k == 5 && g.s == 2) return launch_dw_t<DT, 5, 2>(x, wdw, ep, y, g, st);
+  return set_error(FCM_E_UNSUPPORTED, "dw: only k in {3,5} and stride in {1,2} are built");
+}
+
+int launch_dw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  switch (dt) {
+    case FCM_F32: return launch_dw_dt<FCM_F32>(x, wdw, ep, y, g, st);
+    case FCM_BF16: return launch_dw_dt<FCM_BF16>(x, wdw, ep, y, g, st);
+    case FCM_F16: return launch_dw_dt<FCM_F16>(x, wdw, ep, y, g, st);
+    case FCM_S8: return launch_dw_dt<FCM_S8>(x, wdw, ep, y, g, st);
+  }
+  return set_error(FCM_E_INVAL, "bad dtype");
+}
+
+template <int DT>
+static int launch_dw_nchw_t(const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  using TT = typename Tr<DT>::T;
+  const long long total = (long long)g.N * g.C * g.Ho * g.Wo;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)device_props().sms * 16);
+  dw_nchw_kernel<DT><<<blocks, 256, 0, st>>>(static_cast<const TT*>(x), static_cast<const TT*>(wdw), ep,
+                                             static_cast<TT*>(y), g.C, g.H, g.W, g.Ho, g.Wo, g.k, g.s, g.pt, g.pl,
+                                             total);
+  return check_launch("dw_nchw_kernel");
+}
+
+int launch_dw_nchw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  switch (dt) {
+    case FCM_F32: return launch_dw_nchw_t<FCM_F32>(x, wdw, ep, y, g, st);
+    case FCM_BF16: return launch_dw_nchw_t<FCM_BF16>(x, wdw, ep, y, g, st);
+    case FCM_F16: return launch_dw_nchw_t<FCM_F16>(x, wdw, ep, y, g, st);
+    case FCM_S8: return launch_dw_nchw_t<FCM_S8>(x, wdw, ep, y, g, st);
+  }
+  return set_error(FCM_E_INVAL, "bad dtype");
+}
+
+int launch_pack_pw(int dt, int cin, int cout, const void* w, void* packed, cudaStream_t st) {
+  dim3 grid((cout + 31) / 32, (cin + 31) / 32), block(32, 8);
+  switch (elem_size(dt)) {
+    case 4: pack_pw_kernel<uint32_t><<<grid, block, 0, st>>>((const uint32_t*)w, (uint32_t*)packed, cin, cout); break;
+    case 2: pack_pw_kernel<uint16_t><<<grid, block, 0, st>>>((const uint16_t*)w, (uint16_t*)packed, cin, cout); break;
+    default: pack_pw_kernel<uint8_t><<<grid, block, 0, st>>>((const uint8_t*)w, (uint8_t*)packed, cin, cout); break;
+  }
+  return check_launch("pack_pw_kernel");
+}
+
+}  // namespace fcm

@@ -1,0 +1,58 @@
+// Host-side internals of libfcm.so (not part of the public ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "fcm.h"
+
+namespace fcm {
+
+struct Epi;  // common.cuh
+
+// thread-local error detail + status helper
+int set_error(int status, const std::string& msg);
+extern std::atomic<uint64_t> g_launches;
+
+struct DevProps {
+  int sms = 148;
+  int smem_optin = 232448;
+  int l2_bytes = 126 * 1024 * 1024;
+  int cc_major = 10, cc_minor = 0;
+};
+const DevProps& device_props();  // cached per process (device of the calling thread at first use)
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+bool encode_tmap(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* base, const uint64_t* dims,
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz);
+CUtensorMapDataType tmap_dtype(int dt);
+int elem_size(int dt);
+
+// Tile geometry resolved for a launch.
+struct Geo {
+  int N, H, W, C, Ho, Wo, Cout;   // Cout: PW output (DWPW) or C_mid (PWDW)
+  int k, s, pt, pl;
+  int nb, th, tw;                 // images x rows x cols per output tile
+};
+
+// launchers (return FCM_OK or an FCM_E_* code; all validation already done by the API layer)
+int launch_dw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
+int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st);
+int launch_pw_simt(const float* x, const float* wp, const Epi& ep, float* y, int M, int K, int N, cudaStream_t st);
+int launch_dwpw_tc(int dt, const void* x, const void* wdw, const Epi& ed, const void* wp, const Epi& ep, void* y,
+                   const Geo& g, int n_split, cudaStream_t st);
+int launch_dwpw_simt(const float* x, const float* wdw, const Epi& ed, const float* wp, const Epi& ep, float* y,
+                     const Geo& g, cudaStream_t st);
+int launch_pwdw_tc(int dt, const void* x, const void* wp, const Epi& ep, const void* wdw, const Epi& ed, void* y,
+                   const Geo& g, cudaStream_t st);
+int launch_pwdw_simt(const float* x, const float* wp, const Epi& ep, const float* wdw, const Epi& ed, float* y,
+                     const Geo& g, cudaStream_t st);
+int launch_pack_pw(int dt, int cin, int cout, const void* w, void* packed, cudaStream_t st);
+int launch_dw_nchw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
+
+int check_launch(const char* what);
+
+}  // namespace fcm

@@ -1,0 +1,126 @@
+"""CUDA path vs the oracle, element by element, on seeded inputs (through the C ABI).
+
+Sizes span several tiles, ragged spatial/channel tails, both strides, k=3/5, every dtype.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.cases import Case, as_np, compare, stored
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------- configs[0]: the single DWPW layer
+@pytest.mark.parametrize("fmt", ["f32", "s8", "bf16", "f16"])
+def test_config0_single_dwpw(fmt):
+    Case("dwpw", fmt, 1, 14, 14, 16, 32, k=3, s=1).check()
+
+
+@pytest.mark.parametrize("fmt", ["f32", "s8", "bf16"])
+def test_config0_unfused_layers(fmt):
+    Case("dw", fmt, 1, 14, 14, 16, k=3, s=1).check()
+    Case("pw", fmt, 1, 14, 14, 16, 32).check()
+
+
+# ---------------------------------------------------------------- DW
+@pytest.mark.parametrize("fmt", ["f32", "bf16", "f16", "s8"])
+@pytest.mark.parametrize("k,s", [(3, 1), (3, 2), (5, 1), (5, 2)])
+def test_dw(fmt, k, s):
+    c = 160 if fmt == "s8" else 80
+    Case("dw", fmt, 2, 23, 29, c, k=k, s=s).check()
+
+
+def test_dw_asymmetric_pads_and_tiny():
+    Case("dw", "bf16", 1, 1, 1, 16, k=3, s=1).check()
+    Case("dw", "bf16", 2, 12, 12, 24, k=3, s=2, pads=(0, 0, 1, 1)).check()
+    Case("dw", "s8", 1, 9, 7, 32, k=5, s=1, pads=(1, 2, 3, 0)).check()
+
+
+def test_dw_nchw():
+    import paper_2404_19331_b200 as fcm
+    c = Case("dw", "bf16", 2, 11, 13, 24, k=3, s=2)
+    ref, mag = c.oracle()
+    from tests.cases import device_epi
+    x = c.x.permute(0, 3, 1, 2).contiguous().cuda()
+    y = fcm.dw(x, stored(c.pd["w"], "bf16").cuda(), 2, None, device_epi(c.pd, "bf16", "cuda"), layout="nchw")
+    compare(as_np(y.permute(0, 2, 3, 1), "bf16"), ref, mag, "bf16", "dw nchw")
+
+
+# ---------------------------------------------------------------- PW
+@pytest.mark.parametrize("fmt", ["f32", "bf16", "f16", "s8"])
+@pytest.mark.parametrize("c_in,c_out", [(16, 32), (40, 24), (144, 24), (320, 1280), (96, 576)])
+def test_pw(fmt, c_in, c_out):
+    if fmt == "s8" and (c_in % 16 or c_out % 16):
+        pytest.skip("int8 needs 16-byte channel pitch")
+    Case("pw", fmt, 2, 13, 11, c_in, c_out).check()
+
+
+# ---------------------------------------------------------------- FCM DWPW
+@pytest.mark.parametrize("fmt", ["bf16", "f16", "s8", "f32"])
+@pytest.mark.parametrize("k,s", [(3, 1), (3, 2), (5, 1), (5, 2)])
+def test_dwpw(fmt, k, s):
+    c_in, c_out = (160, 48) if fmt == "s8" else (96, 40)
+    Case("dwpw", fmt, 3, 23, 21, c_in, c_out, k=k, s=s).check()
+
+
+@pytest.mark.parametrize("shape", [(4, 7, 7, 160, 320), (2, 14, 14, 576, 96), (1, 28, 28, 32, 16),
+                                   (2, 56, 56, 144, 24)])
+def test_dwpw_network_shapes_bf16(shape):
+    n, h, w, ci, co = shape
+    Case("dwpw", "bf16", n, h, w, ci, co, k=3, s=1).check()
+
+
+def test_dwpw_explicit_tiles_and_splits():
+    for tile in [dict(tile_h=4, tile_w=8), dict(tile_h=8, tile_w=16, n_split=2), dict(tile_h=7, tile_w=7, tile_n=2)]:
+        Case("dwpw", "bf16", 3, 14, 14, 64, 96, tile=tile).check()
+
+
+# ---------------------------------------------------------------- FCM PWDW_R
+@pytest.mark.parametrize("fmt", ["bf16", "f16", "s8", "f32"])
+@pytest.mark.parametrize("k,s", [(3, 1), (3, 2), (5, 1), (5, 2)])
+def test_pwdw_r(fmt, k, s):
+    c_in, c_mid = (32, 144) if fmt == "s8" else (24, 72)
+    Case("pwdw", fmt, 2, 19, 17, c_in, c_mid, k=k, s=s).check()
+
+
+def test_pwdw_r_border_trap_nonzero_bias():
+    """PW bias is nonzero -> T must be zero-padded, not eps_pw(PW(0)) (reading R6)."""
+    c = Case("pwdw", "bf16", 1, 9, 9, 16, 64, k=3, s=1)
+    c.pp["bias"] = np.full_like(c.pp["bias"], 0.75)
+    c.check()
+
+
+def test_pwdw_r_tiling_invariance_bitwise():
+    outs = []
+    for tile in [None, dict(tile_h=4, tile_w=4), dict(tile_h=7, tile_w=3), dict(tile_h=14, tile_w=14)]:
+        c = Case("pwdw", "bf16", 2, 14, 14, 32, 64, k=3, s=1, tile=tile)
+        outs.append(c.gpu())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+# ---------------------------------------------------------------- GPU self-consistency
+def test_int8_fused_equals_unfused_bitwise():
+    import paper_2404_19331_b200 as fcm
+    from tests.cases import device_epi
+    c = Case("dwpw", "s8", 2, 20, 20, 64, 48, k=3, s=2)
+    x = c.x.cuda()
+    wdw, ed = stored(c.pd["w"], "s8").cuda(), device_epi(c.pd, "s8", "cuda")
+    wpk, ep = fcm.pack_pw(stored(c.pp["w"], "s8").cuda()), device_epi(c.pp, "s8", "cuda")
+    fused = fcm.dwpw(x, wdw, 2, None, ed, wpk, ep)
+    unfused = fcm.pw(fcm.dw(x, wdw, 2, None, ed), wpk, ep)
+    assert torch.equal(fused, unfused)
+
+
+# ---------------------------------------------------------------- error behaviour
+def test_abi_errors_on_gpu():
+    import paper_2404_19331_b200 as fcm
+    from paper_2404_19331_b200._lib import FcmError
+    x = torch.zeros(1, 8, 8, 24, dtype=torch.int8, device="cuda")  # 24-byte pitch: not 16-B aligned
+    w = torch.zeros(3, 3, 24, dtype=torch.int8, device="cuda")
+    ep = fcm.Epilogue(mult_q=torch.ones(24, dtype=torch.int32, device="cuda"),
+                      shift_q=torch.ones(24, dtype=torch.int32, device="cuda"))
+    with pytest.raises(FcmError) as e:
+        fcm.dw(x, w, 1, None, ep)
+    assert e.value.status == -2
