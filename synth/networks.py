@@ -94,3 +94,40 @@ NETWORKS = {
     "efficientnet_b0": efficientnet_b0,
     "cvt13": cvt13_projections,
 }
+
+
+def layer_ids(blocks):
+    """[(id, block index, layer dict)] in execution order; ids are 'b<block>.<i>'."""
+    return [(f"b{bi}.{li}", bi, l) for bi, b in enumerate(blocks) for li, l in enumerate(b)]
+
+
+def network_params(seed: int, net: str, dtype: str) -> dict:
+    """Per-layer synthetic parameters of a network (numpy; weights NOT yet cast to the storage
+    dtype). int8 requantisers assume sigma_in = 73.9 for the first layer and 32 afterwards."""
+    import synth
+    out = {}
+    sigma = 73.9
+    for lid, _, l in layer_ids(NETWORKS[net]()):
+        name = f"{net}/{lid}"
+        if dtype == "s8":
+            if l["kind"] == "dw":
+                p = synth.int8_dw_params(seed, name, l["k"], l["c"], l["act"], sigma)
+            else:
+                p = synth.int8_pw_params(seed, name, l["c_in"], l["c_out"], l["act"], sigma)
+            sigma = 32.0
+        else:
+            if l["kind"] == "dw":
+                p = synth.float_dw_params(seed, name, l["k"], l["c"], l["act"])
+            else:
+                p = synth.float_pw_params(seed, name, l["c_in"], l["c_out"], l["act"])
+        out[lid] = p
+    return out
+
+
+def block_source(net: str, blocks, bi: int):
+    """Where block bi reads its input: ('chain', None) = previous block's output, or
+    ('stage', role) = a stage token map shared by all CvT projections of that stage."""
+    if net != "cvt13":
+        return ("chain", None)
+    l = blocks[bi][0]
+    return ("stage", f"{net}/stage_{l['h']}x{l['c']}")
