@@ -188,6 +188,15 @@ def pred_us(c, dtype, g):
     return max(max(hbm, l2), max(dw, pw)) + g["launch_us"]
 
 
+def _bn(co, ns, b):
+    """PW column block of the tensor-core kernels: one block padded to 16 when ns == 1, else a
+    multiple of the 128-byte store chunk (128/b columns), at most 256."""
+    if ns == 1:
+        return (co + 15) // 16 * 16
+    cpc = 128 // b
+    return min((ceil(co / ns) + cpc - 1) // cpc * cpc, 256)
+
+
 def b200_numbers(op, layers, N, dtype, tile):
     """Compulsory HBM bytes, exact L2->SM bytes and MACs of one candidate at its reported tile."""
     b = ESZ[dtype]
@@ -204,9 +213,7 @@ def b200_numbers(op, layers, N, dtype, tile):
         M = N * p["h"] * p["w"]
         ci, co = p["c_in"], p["c_out"]
         bm = th
-        bn = ceil(co / ns)
-        if dtype != "f32":
-            bn = (bn + 15) // 16 * 16
+        bn = 64 if dtype == "f32" else _bn(co, ns, b)
         u = pw_units(M, ci, co, bm, bn)
         return dict(dram_bytes=(M * (ci + co) + ci * co) * b, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
                     dw_macs=0, pw_macs=M * ci * co, redundant_macs=0)
@@ -214,7 +221,7 @@ def b200_numbers(op, layers, N, dtype, tile):
         d, p = layers
         Ho, Wo = out_hw(d)
         ci, co = d["c"], p["c_out"]
-        bn = 64 if dtype == "f32" else (ceil(co / ns) + 15) // 16 * 16
+        bn = 64 if dtype == "f32" else _bn(co, ns, b)
         u = units("dwpw", N, d, ci, co, nb, th, tw, bn)
         dram = (N * (d["h"] * d["w"] * ci + Ho * Wo * co) + d["k"] ** 2 * ci + ci * co) * b
         return dict(dram_bytes=dram, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,

@@ -62,11 +62,10 @@ template <> struct Tr<FCM_S8> {
 };
 
 // ---------------------------------------------------------------------------- epilogue
-__device__ __forceinline__ float act_f(float v, int act) {
-  if (act == FCM_ACT_RELU) return fmaxf(v, 0.f);
-  if (act == FCM_ACT_RELU6) return fminf(fmaxf(v, 0.f), 6.f);
-  return v;
-}
+// Activation as a clamp [lo, hi] (NONE: (-inf, inf), RELU: [0, inf), RELU6: [0, 6]); branch-free.
+__device__ __forceinline__ float act_lo(int act) { return act == FCM_ACT_NONE ? -INFINITY : 0.f; }
+__device__ __forceinline__ float act_hi(int act) { return act == FCM_ACT_RELU6 ? 6.f : INFINITY; }
+__device__ __forceinline__ float act_f(float v, int act) { return fminf(fmaxf(v, act_lo(act)), act_hi(act)); }
 
 // Per-channel epilogue constants held in registers.
 struct EpiC {
@@ -150,46 +149,130 @@ __device__ __forceinline__ void load_dw_weights(DwW<DT, K>& W, const typename Tr
       }
 }
 
-// ---------------------------------------------------------------------------- DW column core
-// One output column of a tile: rows [0, nrows) at stride S over a K x K window that slides down
-// the staged input. `src` points at the lane's 32-bit word of input pixel (row 0, col x*S) in
-// shared memory; consecutive input columns are `col_words` words apart and consecutive input
-// rows `row_words` apart. sink(y, acc) receives the VEC accumulators of output row y.
-// Each input word is read from shared memory once per column and reused for K (or K/S) taps.
+// Per-column epilogue constants staged once per CTA in shared memory (broadcast reads through
+// explicit ld.shared). float: scale[ncap], bias[ncap]; int8: bias_q, mult_q, shift_q [ncap].
+struct EpiS {
+  uint32_t base;  // shared-space byte address
+  int ncap;
+  __device__ __forceinline__ float sc(int n) const { return __uint_as_float(lds32(base + 4 * n)); }
+  __device__ __forceinline__ float bi(int n) const { return __uint_as_float(lds32(base + 4 * (ncap + n))); }
+  __device__ __forceinline__ int32_t bq(int n) const { return (int32_t)lds32(base + 4 * n); }
+  __device__ __forceinline__ int32_t mq(int n) const { return (int32_t)lds32(base + 4 * (ncap + n)); }
+  __device__ __forceinline__ int32_t sh(int n) const { return (int32_t)lds32(base + 4 * (2 * ncap + n)); }
+};
+
+// Fill the constant arrays for columns [0, ncap) (zeros past N).
+template <int DT>
+__device__ __forceinline__ EpiS stage_consts(const Epi& e, int N, int ncap, uint8_t* area) {
+  if constexpr (DT == FCM_S8) {
+    int32_t* bq = reinterpret_cast<int32_t*>(area);
+    int32_t* mq = bq + ncap;
+    int32_t* sh = mq + ncap;
+    for (int i = threadIdx.x; i < ncap; i += blockDim.x) {
+      const bool v = i < N;
+      bq[i] = (v && e.bias_q) ? e.bias_q[i] : 0;
+      mq[i] = v ? e.mult_q[i] : 0;
+      sh[i] = v ? e.shift_q[i] : 1;
+    }
+  } else {
+    float* sc = reinterpret_cast<float*>(area);
+    float* bi = sc + ncap;
+    for (int i = threadIdx.x; i < ncap; i += blockDim.x) {
+      const bool v = i < N;
+      sc[i] = v ? (e.scale ? e.scale[i] : 1.f) : 0.f;
+      bi[i] = (v && e.bias) ? e.bias[i] : 0.f;
+    }
+  }
+  return EpiS{smem_u32(area), ncap};
+}
+template <int DT> constexpr int consts_bytes(int ncap) { return (DT == FCM_S8 ? 12 : 8) * ncap; }
+
+template <int DT>
+__device__ __forceinline__ EpiC epic(const EpiS& cs, int c) {
+  if constexpr (DT == FCM_S8) return EpiC{0.f, 0.f, cs.bq(c), cs.mq(c), cs.sh(c)};
+  else return EpiC{cs.sc(c), cs.bi(c), 0, 0, 1};
+}
+
+// ---------------------------------------------------------------------------- DW segment core
+// Output rows [y0, y0+nrows) of one output column of a staged tile. `src` points at the lane's
+// 32-bit word of input pixel (row 0, col x*S) in shared memory; input columns are `col_words`
+// words apart, rows `row_words` apart; input rows are clamped to `max_row` (the tile's last
+// staged row: rows computed past the tile are never stored). Rows are produced R at a time from
+// a K x K window that slides down the column, so each staged word is read about once and the
+// R x VEC accumulation chains are independent (ILP). Tap order (i, j) is fixed, so every
+// kernel that uses this core produces bit-identical DW results.
+template <int DT, int K> constexpr int dw_rows_per_step() { return (K == 3 && Tr<DT>::VEC <= 2) ? 4 : 1; }
+
 template <int DT, int K, int S, class Sink>
-__device__ __forceinline__ void dw_column(const uint32_t* src, int col_words, int row_words, int nrows,
-                                         const DwW<DT, K>& W, Sink&& sink) {
+__device__ __forceinline__ void dw_segment(uint32_t src, int col_bytes, int row_bytes, int y0, int nrows,
+                                           int max_row, const DwW<DT, K>& W, Sink&& sink) {
   using A = typename Tr<DT>::acc_t;
   constexpr int V = Tr<DT>::VEC;
-  A win[K][K][V];
+  constexpr int R = dw_rows_per_step<DT, K>();
+  constexpr int WR = (R - 1) * S + K;  // window rows
+  A win[WR][K][V];
+  int r0 = y0 * S;  // input row of window row 0
 #pragma unroll
-  for (int i = 0; i < K; ++i)
+  for (int i = 0; i < WR; ++i) {
+    const uint32_t rp = src + min(r0 + i, max_row) * row_bytes;
 #pragma unroll
-    for (int j = 0; j < K; ++j) Tr<DT>::unpack(src[i * row_words + j * col_words], win[i][j]);
-  for (int y = 0; y < nrows; ++y) {
+    for (int j = 0; j < K; ++j) Tr<DT>::unpack(lds32(rp + j * col_bytes), win[i][j]);
+  }
+  for (int y = 0; y < nrows; y += R) {
     if (y > 0) {
+      r0 += R * S;
+      constexpr int KEEP = WR - R * S > 0 ? WR - R * S : 0;
 #pragma unroll
-      for (int i = 0; i < K - S; ++i)
+      for (int i = 0; i < KEEP; ++i)
 #pragma unroll
         for (int j = 0; j < K; ++j)
 #pragma unroll
-          for (int v = 0; v < V; ++v) win[i][j][v] = win[i + S][j][v];
-      const uint32_t* r = src + (y * S) * row_words;
+          for (int v = 0; v < V; ++v) win[i][j][v] = win[i + R * S][j][v];
 #pragma unroll
-      for (int i = K - S; i < K; ++i)
+      for (int i = KEEP; i < WR; ++i) {
+        const uint32_t rp = src + min(r0 + i, max_row) * row_bytes;
 #pragma unroll
-        for (int j = 0; j < K; ++j) Tr<DT>::unpack(r[i * row_words + j * col_words], win[i][j]);
+        for (int j = 0; j < K; ++j) Tr<DT>::unpack(lds32(rp + j * col_bytes), win[i][j]);
+      }
     }
-    A acc[V];
+    A acc[R][V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) acc[v] = 0;
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[r][v] = 0;
 #pragma unroll
     for (int i = 0; i < K; ++i)
 #pragma unroll
       for (int j = 0; j < K; ++j)
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[v] += win[i][j][v] * W.w[i][j][v];
-    sink(y, acc);
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[r][v] += win[r * S + i][j][v] * W.w[i][j][v];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (y + r < nrows) sink(y0 + y + r, acc[r]);
+  }
+}
+
+// Load this lane's DW weights from a shared-memory copy of Wdw laid out [k*k][C/VEC words].
+template <int DT, int K>
+__device__ __forceinline__ void load_dw_weights_smem(DwW<DT, K>& W, const uint32_t* wsm, int cwords, int cw) {
+  const uint32_t a = smem_u32(wsm) + 4 * cw;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) Tr<DT>::unpack(lds32(a + 4 * (i * K + j) * cwords), W.w[i][j]);
+}
+
+// Copy Wdw [k*k][C] (global) into shared memory as [k*k][cwords] 32-bit words, zero-padding
+// channel words >= C/VEC up to cwords.
+template <int DT>
+__device__ __forceinline__ void stage_dw_weights(const void* wdw, int k, int C, int cwords, uint32_t* wsm) {
+  const uint32_t* g = static_cast<const uint32_t*>(wdw);
+  const int cw_real = C / Tr<DT>::VEC;
+  for (int i = threadIdx.x; i < k * k * cwords; i += blockDim.x) {
+    const int t = i / cwords, w = i - t * cwords;
+    wsm[i] = (w < cw_real) ? g[t * cw_real + w] : 0u;
   }
 }
 

@@ -52,13 +52,14 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
   for (int col = warp; col < tw; col += 4) {
     const int x = x0 + col;
     if (x >= Wo) break;
-    const uint32_t* src = xs + (col * S) * 32 + lane;
-    dw_column<DT, K, S>(src, 32, tw_in * 32, nrows, W, [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
-      if (c < C) {
-        const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
-        yw[(pix * C + c) / V] = epi_pack<DT>(acc, ec, ep);
-      }
-    });
+    const uint32_t src = smem_u32(xs) + ((col * S) * 32 + lane) * 4;
+    dw_segment<DT, K, S>(src, 128, tw_in * 128, 0, nrows, th_in - 1, W,
+                         [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
+                           if (c < C) {
+                             const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
+                             yw[(pix * C + c) / V] = epi_pack<DT>(acc, ec, ep);
+                           }
+                         });
   }
 }
 

@@ -264,8 +264,8 @@ static Cost b200_pw(const Layer& p, ll N, int dt, ll b, const Gpu& gp) {
   if (dt == FCM_F32) {
     bm = 64; bn = 64;
   } else {
-    const ll nbn = cdiv(p.Cout, 256);
-    bn = (cdiv(p.Cout, nbn) + 15) / 16 * 16;
+    int nb_out = 0;
+    bn = pick_bn((int)p.Cout, 0, (int)(128 / b), nb_out);
   }
   c.th = bm; c.nsplit = cdiv(p.Cout, bn);
   const Units u = pw_units(M, p.C, p.Cout, bm, bn);
@@ -286,8 +286,8 @@ static Cost b200_dwpw(const Layer& d, const Layer& p, ll N, int dt, ll b, const 
     g.nb = 1; g.th = 8; g.tw = 8; bn = 64;
   } else {
     default_dwpw_tile(g);
-    const ll ns = cdiv(Co, 256);
-    bn = (cdiv(Co, ns) + 15) / 16 * 16;
+    int nb_out = 0;
+    bn = pick_bn((int)Co, 0, (int)(128 / b), nb_out);
     if (!dwpw_tile_ok(g, g.nb, g.th, g.tw)) return c;
   }
   c.ok = true;

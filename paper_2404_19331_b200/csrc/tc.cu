@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "host.h"
+#include "tiles.h"
 
 namespace fcm {
 
@@ -26,10 +27,10 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// Epilogue of 16 accumulator columns of one output row -> packed storage words.
-// Returns the number of 32-bit words written into out[] (16 / VEC).
+// Epilogue of 16 accumulator columns [n_base, n_base+16) of one row -> packed storage words.
 template <int DT>
-__device__ __forceinline__ void epi16(const uint32_t (&r)[16], const Epi& e, int n_base, int N, uint32_t (&out)[8]) {
+__device__ __forceinline__ void epi16(const uint32_t (&r)[16], const EpiS& cs, const Epi& e, int n_base,
+                                      uint32_t (&out)[8]) {
   if constexpr (DT == FCM_S8) {
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -37,11 +38,8 @@ __device__ __forceinline__ void epi16(const uint32_t (&r)[16], const Epi& e, int
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int n = n_base + 4 * w + i;
-        int32_t q = 0;
-        if (n < N) {
-          EpiC c{0.f, 0.f, e.bias_q ? __ldg(e.bias_q + n) : 0, __ldg(e.mult_q + n), __ldg(e.shift_q + n)};
-          q = requant_i8(static_cast<int32_t>(r[4 * w + i]), c, e.zp_out, e.qmin, e.qmax);
-        }
+        EpiC c{0.f, 0.f, cs.bq(n), cs.mq(n), cs.sh(n)};
+        const int32_t q = requant_i8(static_cast<int32_t>(r[4 * w + i]), c, e.zp_out, e.qmin, e.qmax);
         word |= (static_cast<uint32_t>(q) & 0xFFu) << (8 * i);
       }
       out[w] = word;
@@ -49,71 +47,100 @@ __device__ __forceinline__ void epi16(const uint32_t (&r)[16], const Epi& e, int
   } else {
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      float v[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int n = n_base + 2 * w + i;
-        float sc = 1.f, bi = 0.f;
-        if (n < N) {
-          sc = e.scale ? __ldg(e.scale + n) : 1.f;
-          bi = e.bias ? __ldg(e.bias + n) : 0.f;
-        }
-        v[i] = epi_f(__uint_as_float(r[2 * w + i]), sc, bi, e.act);
-      }
+      const int n = n_base + 2 * w;
+      const float v0 = epi_f(__uint_as_float(r[2 * w]), cs.sc(n), cs.bi(n), e.act);
+      const float v1 = epi_f(__uint_as_float(r[2 * w + 1]), cs.sc(n + 1), cs.bi(n + 1), e.act);
       if constexpr (DT == FCM_BF16) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(v[0], v[1]);
+        __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
         out[w] = *reinterpret_cast<uint32_t*>(&h);
       } else {
-        __half2 h = __floats2half2_rn(v[0], v[1]);
+        __half2 h = __floats2half2_rn(v0, v1);
         out[w] = *reinterpret_cast<uint32_t*>(&h);
       }
     }
   }
 }
 
-// Store the 16 outputs of columns [n_base, n_base+16) of row `row_ptr` (16-byte vectors,
-// skipping vectors past N). N*ES is a multiple of 16 (validated).
-template <int DT>
-__device__ __forceinline__ void store16(uint8_t* row_ptr, const uint32_t (&o)[8], int n_base, int N) {
+// Byte offset of 16-byte vector `vi` (0..7) of row m in a SWIZZLE_128B tile (1024-B aligned).
+__device__ __forceinline__ uint32_t sw128_vec(int m, int vi) {
+  return (m >> 3) * 1024 + (m & 7) * 128 + ((vi ^ (m & 7)) << 4);
+}
+
+// Epilogue of one TMEM accumulator tile (128 lanes x BN columns) by NEPI warps (4 or 8; warp w
+// reads lane quadrant w%4 and every (NEPI/4)-th 16-column subchunk). Each 128-byte chunk of
+// output columns is converted into a SWIZZLE_128B staging tile (two buffers, alternating) and
+// written by ONE TMA store issued by thread 0: full-line, coalesced HBM writes; rows / columns
+// outside the tensor are clipped by the TMA unit.
+template <int DT, int NEPI, class StoreFn>
+__device__ __forceinline__ void epilogue_tile(uint32_t tacc, int BN, int n0, int N, const EpiS& cs, const Epi& e,
+                                              uint8_t* stage, int& sbuf, StoreFn&& store) {
   constexpr int ES = Tr<DT>::ES;
-  constexpr int EPV = 16 / ES;  // elements per 16-byte vector
-  constexpr int NV = 16 / EPV;
+  constexpr int CPC = 128 / ES;  // output columns per 128-byte chunk
+  constexpr int SUB = CPC / 16;  // 16-column subchunks per chunk
+  constexpr int G = NEPI / 4;    // warps sharing a lane quadrant
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, h = warp >> 2;
+  const int m = q * 32 + lane;
+  const int valid = min(BN, N - n0);
+  const int nch = (valid + CPC - 1) / CPC;
+  for (int cc = 0; cc < nch; ++cc, ++sbuf) {
+    uint8_t* buf = stage + (sbuf & 1) * 16384;
+    if (threadIdx.x == 0) bulk_wait_read<1>();
+    named_bar_sync(1, NEPI * 32);
+    for (int j = h; j < SUB; j += G) {
+      const int c0 = cc * CPC + j * 16;
+      if (c0 >= BN) break;
+      uint32_t r[16];
+      tmem_ld16(tacc + ((uint32_t)(q * 32) << 16) + c0, r);
+      tmem_ld_wait();
+      uint32_t o[8];
+      epi16<DT>(r, cs, e, n0 + c0, o);
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    if (n_base + v * EPV < N)
-      *reinterpret_cast<uint4*>(row_ptr + (size_t)(n_base + v * EPV) * ES) =
-          make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+      for (int v = 0; v < ES; ++v)
+        sts128(smem_u32(buf) + sw128_vec(m, j * ES + v), o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, NEPI * 32);
+    if (threadIdx.x == 0) {
+      store(buf, n0 + cc * CPC);
+      bulk_commit();
+    }
   }
 }
 
 // =====================================================================================
-// LBL PW: Y[M,N] = eps(X[M,K] . Wp[N,K]^T). Warps 0-3 epilogue, 4 TMA, 5 MMA.
+// LBL PW: Y[M,N] = eps(X[M,K] . Wp[N,K]^T). Warps 0-7 epilogue, 8 TMA producer, 9 MMA.
 // =====================================================================================
 template <int DT>
-__global__ void __launch_bounds__(192, 1)
-    pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, Epi ep,
-                 uint8_t* __restrict__ y, int M, int N, int K, int BN, int nbn, int stages, uint32_t tmem_cols) {
+__global__ void __launch_bounds__(320, 1)
+    pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+                 const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, int stages,
+                 uint32_t tmem_cols, int ncap) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* abuf = smem;
-  uint8_t* bbuf = smem + stages * 16384;
-  uint64_t* full = reinterpret_cast<uint64_t*>(bbuf + stages * BN * 128);
+  uint8_t* stage = smem;                         // 2 x 16 KB output staging
+  uint8_t* abuf = smem + 32768;
+  uint8_t* bbuf = abuf + stages * 16384;
+  uint8_t* cst = bbuf + stages * BN * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(cst + consts_bytes<DT>(ncap));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 4 && lane == 0) {
+  const EpiS cs = stage_consts<DT>(ep, N, ncap, cst);
+  if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tma);
     tma_prefetch_desc(&tmb);
+    tma_prefetch_desc(&tmy);
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 128); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 256); }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc_rt(tslot, tmem_cols);
+  if (warp == 9) tmem_alloc_rt(tslot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -123,7 +150,7 @@ __global__ void __launch_bounds__(192, 1)
   const int total = nbm * nbn;
   const uint32_t stage_tx = 16384 + BN * 128;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -138,7 +165,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, BN);
       int it = 0, local = 0;
@@ -161,30 +188,21 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    int local = 0;
+    int local = 0, sbuf = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int acc = local & 1;
       const int m0 = (t / nbn) * 128, n0 = (t % nbn) * BN;
       mbar_wait(tfull + acc, (local >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + warp * 32 + lane;
-      uint8_t* rp = y + (size_t)row * N * ES;
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tbase + ((uint32_t)(warp * 32) << 16) + acc * BN + c0, r);
-        tmem_ld_wait();
-        if (n0 + c0 < N && row < M) {
-          uint32_t o[8];
-          epi16<DT>(r, ep, n0 + c0, N, o);
-          store16<DT>(rp, o, n0 + c0, N);
-        }
-      }
+      epilogue_tile<DT, 8>(tbase + acc * BN, BN, n0, N, cs, ep, stage, sbuf,
+                           [&](const uint8_t* buf, int c) { tma_store_2d(&tmy, buf, c, m0); });
       tc_fence_before();
       mbar_arrive(tempty + acc);
     }
+    if (threadIdx.x == 0) bulk_wait_all();
   }
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc_rt(tbase, tmem_cols);
   }
@@ -201,11 +219,11 @@ constexpr int kDwpwNDW = 8;
 template <int DT, int K, int S>
 __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
     dwpw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
-                   const typename Tr<DT>::T* __restrict__ wdw, Epi ed, Epi ep, uint8_t* __restrict__ y, int N,
-                   int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw, int tiles_x,
-                   int tiles_y, int nsplit, int BN, int stages, uint32_t tmem_cols) {
-  constexpr int ES = Tr<DT>::ES;
+                   const __grid_constant__ CUtensorMap tmy, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
+                   Epi ep, int N, int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw,
+                   int tiles_x, int tiles_y, int nsplit, int BN, int stages, uint32_t tmem_cols, int ncap) {
   constexpr int V = Tr<DT>::VEC;
+  constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
   constexpr int WARP_TMA = 4 + kDwpwNDW, WARP_MMA = 5 + kDwpwNDW;
@@ -215,16 +233,26 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
   const int stage_bytes = xstride + 16384 + BN * 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint8_t* ostage = smem;                          // 2 x 16 KB output staging
+  uint8_t* sbase = smem + 32768;
+  const int nk = (Cin + KC - 1) / KC;
+  uint8_t* cst = sbase + stages * stage_bytes;
+  uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(nk * KC));  // DW weights
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + K * K * nk * 32);
   uint64_t* afull = full + stages;
   uint64_t* empty = afull + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const EpiS cs = stage_consts<DT>(ep, Cout, ncap, cst);
+  const EpiS dcs = stage_consts<DT>(ed, Cin, nk * KC, dcst);
+  stage_dw_weights<DT>(wdw, K, Cin, nk * 32, wsm);
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
+    tma_prefetch_desc(&tmy);
     for (int s = 0; s < stages; ++s) {
       mbar_init(full + s, 1);
       mbar_init(afull + s, kDwpwNDW * 32);
@@ -238,25 +266,28 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const int nk = (Cin + KC - 1) / KC;
   const int spatial = ((N + nb - 1) / nb) * tiles_y * tiles_x;
   const int total = spatial * nsplit;
+  auto decode = [&](int t, int& ns, int& nbi, int& tyi, int& txi) {
+    ns = t % nsplit;
+    int sp = t / nsplit;
+    txi = sp % tiles_x;
+    sp /= tiles_x;
+    tyi = sp % tiles_y;
+    nbi = sp / tiles_y;
+  };
 
   if (warp == WARP_TMA) {
     if (lane == 0) {
       const uint32_t tx = xbytes + BN * 128;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int ns = t % nsplit;
-        int sp = t / nsplit;
-        const int txi = sp % tiles_x;
-        sp /= tiles_x;
-        const int tyi = sp % tiles_y;
-        const int nbi = sp / tiles_y;
+        int ns, nbi, tyi, txi;
+        decode(t, ns, nbi, tyi, txi);
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % stages;
           mbar_wait(empty + s, ((it / stages) & 1) ^ 1);
-          uint8_t* st = smem + s * stage_bytes;
+          uint8_t* st = sbase + s * stage_bytes;
           mbar_arrive_expect_tx(full + s, tx);
           tma_load_4d(st, &tmx, full + s, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
           tma_load_2d(st + xstride + 16384, &tmb, full + s, kc * KC, ns * BN);
@@ -278,7 +309,7 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
           mbar_wait(full + s, ph);
           mbar_wait(afull + s, ph);
           tc_fence_after();
-          uint8_t* st = smem + s * stage_bytes;
+          uint8_t* st = sbase + s * stage_bytes;
           const uint64_t ad = smem_desc_sw128(smem_u32(st + xstride));
           const uint64_t bd = smem_desc_sw128(smem_u32(st + xstride + 16384));
 #pragma unroll
@@ -290,68 +321,55 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
     }
   } else if (warp >= 4) {
     // ---------------- DW warps: X halo chunk (smem) -> DW -> eps_dw -> A operand (commBuffer)
+    // work item = (output column, segment of kSeg rows), round-robin over the DW warps
+    constexpr int kSeg = 8;
     const int dw = warp - 4;
-    const int ncols = nb * tw;
+    const int nseg = (th + kSeg - 1) / kSeg;
+    const int nitems = nb * tw * nseg;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       for (int kc = 0; kc < nk; ++kc, ++it) {
         const int s = it % stages;
         const int c = kc * KC + lane * V;
         DwW<DT, K> W;
-        load_dw_weights<DT, K>(W, wdw, Cin, c);
+        load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + lane);
         EpiC ec[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ed, c + v, c + v < Cin);
+        for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
         mbar_wait(full + s, (it / stages) & 1);
-        uint8_t* st = smem + s * stage_bytes;
-        const uint32_t* xs = reinterpret_cast<const uint32_t*>(st);
-        uint8_t* abase = st + xstride;
-        for (int col = dw; col < ncols; col += kDwpwNDW) {
+        const uint32_t st = smem_u32(sbase + s * stage_bytes);
+        const uint32_t abase = st + xstride;
+        for (int item = dw; item < nitems; item += kDwpwNDW) {
+          const int col = item / nseg, seg = item - col * nseg;
           const int b = col / tw, x = col - b * tw;
-          const uint32_t* src = xs + ((b * th_in) * tw_in + x * S) * 32 + lane;
-          dw_column<DT, K, S>(src, 32, tw_in * 32, th, W, [&](int yy, const typename Tr<DT>::acc_t(&a)[V]) {
-            const int m = (b * th + yy) * tw + x;
-            const uint32_t word = (c < Cin) ? epi_pack<DT>(a, ec, ed) : 0u;
-            *reinterpret_cast<uint32_t*>(abase + sw128_off(m, lane)) = word;
-          });
+          const int y0 = seg * kSeg;
+          const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
+          dw_segment<DT, K, S>(src, 128, tw_in * 128, y0, min(kSeg, th - y0), th_in - 1, W,
+                               [&](int yy, const typename Tr<DT>::acc_t(&a)[V]) {
+                                 const int m = (b * th + yy) * tw + x;
+                                 const uint32_t word = (c < Cin) ? epi_pack<DT>(a, ec, ed) : 0u;
+                                 sts32(abase + sw128_off(m, lane), word);
+                               });
         }
         fence_proxy_async_smem();
         mbar_arrive(afull + s);
       }
     }
   } else {
-    // ---------------- epilogue warps 0-3: TMEM -> eps_pw -> OFM
-    int local = 0;
+    // ---------------- epilogue warps 0-3: TMEM -> eps_pw -> staging -> TMA store (4-D box)
+    int local = 0, sbuf = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int acc = local & 1;
-      const int ns = t % nsplit;
-      int sp = t / nsplit;
-      const int txi = sp % tiles_x;
-      sp /= tiles_x;
-      const int tyi = sp % tiles_y;
-      const int nbi = sp / tiles_y;
-      const int m = warp * 32 + lane;
-      const int b = m / (th * tw), r = m - b * th * tw;
-      const int yy = r / tw, xx = r - yy * tw;
-      const int n = nbi * nb + b, yo = tyi * th + yy, xo = txi * tw + xx;
-      const bool valid = (b < nb) && (n < N) && (yo < Ho) && (xo < Wo);
-      uint8_t* rp = y + (((size_t)n * Ho + yo) * Wo + xo) * Cout * ES;
-      const int n0 = ns * BN;
+      int ns, nbi, tyi, txi;
+      decode(t, ns, nbi, tyi, txi);
       mbar_wait(tfull + acc, (local >> 1) & 1);
       tc_fence_after();
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t rr[16];
-        tmem_ld16(tbase + ((uint32_t)(warp * 32) << 16) + acc * BN + c0, rr);
-        tmem_ld_wait();
-        if (valid && n0 + c0 < Cout) {
-          uint32_t o[8];
-          epi16<DT>(rr, ep, n0 + c0, Cout, o);
-          store16<DT>(rp, o, n0 + c0, Cout);
-        }
-      }
+      epilogue_tile<DT, 4>(tbase + acc * BN, BN, ns * BN, Cout, cs, ep, ostage, sbuf,
+                           [&](const uint8_t* buf, int c) { tma_store_4d(&tmy, buf, c, txi * tw, tyi * th, nbi * nb); });
       tc_fence_before();
       mbar_arrive(tempty + acc);
     }
+    if (threadIdx.x == 0) bulk_wait_all();
   }
   __syncthreads();
   if (warp == WARP_MMA) {
@@ -361,24 +379,30 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
 }
 
 // =====================================================================================
-// FCM PWDW_R. Warps 0-7: PW epilogue into the smem T tile, then DW from it; warp 8 TMA,
-// warp 9 MMA. One tile = DW output tile (nb x th x tw) x TD intermediate channels (one
-// 128-byte group). The PW runs over the tile's T HALO (R = nb*th_in*tw_in <= 256 rows,
-// 1-2 M=128 MMAs): T pixels in the overlap are recomputed by every tile that needs them
-// (the "_R"). T outside the image is written as 0 (DW pads T, reading R6).
+// FCM PWDW_R. One tile = DW output tile (nb x th x tw) x TD intermediate channels (one 128-byte
+// group). The PW runs over the tile's T HALO (R = nb*th_in*tw_in <= 256 rows, 1-2 M=128 MMAs):
+// T pixels in the overlap are recomputed by every tile that needs them (the "_R"). T
+// outside the image is written as 0 (DW pads T, reading R6).
+// Warps 0-3: T producers (TMEM -> eps_pw -> smem T tile), warps 4-11: DW consumers (T -> DW ->
+// eps_dw -> OFM), warp 12: TMA, warp 13: MMA. TMEM and the T tile are both double-buffered, so
+// the PW of tile i+1, its epilogue and the DW of tile i proceed concurrently.
 // =====================================================================================
+constexpr int kPwdwNDW = 8;
+
 template <int DT, int K, int S>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
     pwdw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                    const typename Tr<DT>::T* __restrict__ wdw, Epi ep, Epi ed, uint8_t* __restrict__ y, int N, int H,
                    int W, int Cin, int Ho, int Wo, int Cmid, int pt, int pl, int nb, int th, int tw, int tiles_x,
-                   int tiles_y, int stages, uint32_t tmem_cols) {
+                   int tiles_y, int stages, uint32_t tmem_cols, int ncap) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int V = Tr<DT>::VEC;
   constexpr int KC = 128 / ES;
   constexpr int TD = 128 / ES;           // intermediate channels per tile
   constexpr int PITCH = 128 + 16;        // bytes per T row in smem (padded: conflict-free)
+  constexpr int PW = PITCH / 4;
   constexpr MmaKind KIND = TcKind<DT>::kind;
+  constexpr int WARP_TMA = 4 + kPwdwNDW, WARP_MMA = 5 + kPwdwNDW;
   const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
   const int R = nb * th_in * tw_in;
   const int MB = (R + 127) / 128;
@@ -386,29 +410,42 @@ __global__ void __launch_bounds__(320, 1)
   const int astride = MB * 16384;
   const int stage_bytes = astride + TD * 128;
   const int tbytes = ((R * PITCH) + 1023) & ~1023;
+  const int nslice = (Cmid + TD - 1) / TD;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* tsm = smem + stages * stage_bytes;  // 2 T buffers
-  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + 2 * tbytes);
+  uint8_t* cst = tsm + 2 * tbytes;
+  uint8_t* dcst = cst + consts_bytes<DT>(ncap);
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(ncap));
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + K * K * nslice * 32);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* Tfull = tempty + 2;
+  uint64_t* Tempty = Tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(Tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 8 && lane == 0) {
+  const EpiS cs = stage_consts<DT>(ep, Cmid, ncap, cst);
+  const EpiS dcs = stage_consts<DT>(ed, Cmid, ncap, dcst);
+  stage_dw_weights<DT>(wdw, K, Cmid, nslice * 32, wsm);
+  if (warp == WARP_TMA && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 256); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 128);
+      mbar_init(Tfull + a, 128);
+      mbar_init(Tempty + a, kPwdwNDW * 32);
+    }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc_rt(tslot, tmem_cols);
+  if (warp == WARP_MMA) tmem_alloc_rt(tslot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
   const int nk = (Cin + KC - 1) / KC;
-  const int nslice = (Cmid + TD - 1) / TD;
   const int spatial = ((N + nb - 1) / nb) * tiles_y * tiles_x;
   const int total = spatial * nslice;
   const uint32_t acc_cols = MB * TD;
@@ -422,7 +459,7 @@ __global__ void __launch_bounds__(320, 1)
     nbi = sp / tiles_y;
   };
 
-  if (warp == 8) {
+  if (warp == WARP_TMA) {
     if (lane == 0) {
       const uint32_t tx = xbytes + TD * 128;
       int it = 0;
@@ -439,7 +476,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == WARP_MMA) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, TD);
       int it = 0, local = 0;
@@ -464,69 +501,83 @@ __global__ void __launch_bounds__(320, 1)
         mma_commit(tfull + acc);
       }
     }
-  } else {
-    const int q = warp & 3, mbw = warp >> 2;
+  } else if (warp < 4) {
+    // ---------------- T producers: TMEM (PW accumulators over the halo) -> eps_pw -> T (0 outside)
+    const int q = warp;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int acc = local & 1;
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       uint8_t* tb = tsm + acc * tbytes;
-      // ---- phase 1: TMEM (PW accumulators over the halo) -> eps_pw -> T tile (zero outside image)
       mbar_wait(tfull + acc, (local >> 1) & 1);
+      mbar_wait(Tempty + acc, ((local >> 1) & 1) ^ 1);
       tc_fence_after();
-      if (mbw < MB) {
-        const int r = mbw * 128 + q * 32 + lane;
+      for (int mb = 0; mb < MB; ++mb) {
+        const int r = mb * 128 + q * 32 + lane;
         const int b = r / (th_in * tw_in), rr = r - b * th_in * tw_in;
         const int yi = tyi * th * S - pt + rr / tw_in, xi = txi * tw * S - pl + rr % tw_in;
         const int n = nbi * nb + b;
         const bool inside = (r < R) && (n < N) && (yi >= 0) && (yi < H) && (xi >= 0) && (xi < W);
         for (int c0 = 0; c0 < TD; c0 += 16) {
           uint32_t rg[16];
-          tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + acc * acc_cols + mbw * TD + c0, rg);
+          tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + acc * acc_cols + mb * TD + c0, rg);
           tmem_ld_wait();
           if (r < R) {
             uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            if (inside) epi16<DT>(rg, ep, sl * TD + c0, Cmid, o);
-            uint8_t* dst = tb + r * PITCH + c0 * ES;
-            constexpr int NV = 16 * ES / 16;
+            if (inside) epi16<DT>(rg, cs, ep, sl * TD + c0, o);
+            const uint32_t dst = smem_u32(tb) + r * PITCH + c0 * ES;
 #pragma unroll
-            for (int v = 0; v < NV; ++v)
-              *reinterpret_cast<uint4*>(dst + 16 * v) = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+            for (int v = 0; v < ES; ++v) sts128(dst + 16 * v, o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
           }
         }
       }
       tc_fence_before();
       mbar_arrive(tempty + acc);
-      named_bar_sync(1, 256);
-      // ---- phase 2: DW over the T tile -> eps_dw -> OFM
+      mbar_arrive(Tfull + acc);
+    }
+  } else {
+    // ---------------- DW consumers: T tile -> DW -> eps_dw -> OFM (128 B per warp store)
+    constexpr int kSeg = 8;
+    const int dw = warp - 4;
+    const int nseg = (th + kSeg - 1) / kSeg;
+    const int nitems = nb * tw * nseg;
+    uint32_t* yw = reinterpret_cast<uint32_t*>(y);
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const int tbi = local & 1;
+      int sl, nbi, tyi, txi;
+      decode(t, sl, nbi, tyi, txi);
       const int c = sl * TD + lane * V;
       DwW<DT, K> Wd;
-      load_dw_weights<DT, K>(Wd, wdw, Cmid, c);
+      load_dw_weights_smem<DT, K>(Wd, wsm, nslice * 32, sl * 32 + lane);
       EpiC ec[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ed, c + v, c + v < Cmid);
-      const uint32_t* tw32 = reinterpret_cast<const uint32_t*>(tb);
-      constexpr int PW = PITCH / 4;
-      uint32_t* yw = reinterpret_cast<uint32_t*>(y);
-      for (int col = warp; col < nb * tw; col += 8) {
+      for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
+      mbar_wait(Tfull + tbi, (local >> 1) & 1);
+      const uint32_t tsa = smem_u32(tsm + tbi * tbytes);
+      const int y0t = tyi * th;
+      const int nrows_t = min(th, Ho - y0t);
+      for (int item = dw; item < nitems; item += kPwdwNDW) {
+        const int col = item / nseg, seg = item - col * nseg;
         const int b = col / tw, x = col - b * tw;
         const int n = nbi * nb + b, xo = txi * tw + x;
-        if (n >= N || xo >= Wo) continue;
-        const int y0 = tyi * th;
-        const int nrows = min(th, Ho - y0);
-        const uint32_t* src = tw32 + ((b * th_in) * tw_in + x * S) * PW + lane;
-        dw_column<DT, K, S>(src, PW, tw_in * PW, nrows, Wd, [&](int yy, const typename Tr<DT>::acc_t(&a)[V]) {
-          if (c < Cmid) {
-            const size_t pix = ((size_t)n * Ho + (y0 + yy)) * Wo + xo;
-            yw[(pix * Cmid + c) / V] = epi_pack<DT>(a, ec, ed);
-          }
-        });
+        const int y0 = seg * kSeg;
+        if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
+        const uint32_t src = tsa + (((b * th_in) * tw_in + x * S) * PW + lane) * 4;
+        dw_segment<DT, K, S>(src, PITCH, tw_in * PITCH, y0, min(kSeg, nrows_t - y0), th_in - 1, Wd,
+                             [&](int yy, const typename Tr<DT>::acc_t(&a)[V]) {
+                               if (c < Cmid) {
+                                 const size_t pix = ((size_t)n * Ho + (y0t + yy)) * Wo + xo;
+                                 yw[(pix * Cmid + c) / V] = epi_pack<DT>(a, ec, ed);
+                               }
+                             });
       }
+      mbar_arrive(Tempty + tbi);
     }
   }
   __syncthreads();
-  if (warp == 9) {
+  if (warp == WARP_MMA) {
     tc_fence_after();
     tmem_dealloc_rt(tbase, tmem_cols);
   }
@@ -541,12 +592,25 @@ static uint32_t pow2_cols(uint32_t c) {
 static inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 template <int DT>
+static int pick_bn(int N, int nsplit, int& nb_out) {
+  return fcm::pick_bn(N, nsplit, 128 / Tr<DT>::ES, nb_out);
+}
+
+static bool out_tmap_2d(CUtensorMap* m, int dt, void* y, int M, int N) {
+  const int ES = elem_size(dt);
+  const uint64_t dims[2] = {(uint64_t)N, (uint64_t)M};
+  const uint64_t str[1] = {(uint64_t)N * ES};
+  const uint32_t box[2] = {(uint32_t)(128 / ES), 128};
+  return encode_tmap(m, tmap_dtype(dt), 2, y, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <int DT>
 static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
-  const int nbn = (N + 255) / 256;
-  const int BN = round_up((N + nbn - 1) / nbn, 16);
-  CUtensorMap ta, tb;
+  int nbn = 0;
+  const int BN = pick_bn<DT>(N, 0, nbn);
+  CUtensorMap ta, tb, ty;
   {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
     const uint64_t str[1] = {(uint64_t)K * ES};
@@ -561,16 +625,20 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
     if (!encode_tmap(&tb, tmap_dtype(DT), 2, wp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return set_error(FCM_E_CUDA, "tensor map (PW B) failed");
   }
+  if (!out_tmap_2d(&ty, DT, y, M, N)) return set_error(FCM_E_CUDA, "tensor map (PW Y) failed");
+  const int ncap = round_up(nbn * BN, 16);
+  const int fixed = 1024 + 32768 + consts_bytes<DT>(ncap) + 256;
   const int stage_bytes = 16384 + BN * 128;
-  const int budget = device_props().smem_optin - 2048;
-  int stages = std::min(8, budget / stage_bytes);
+  const int budget = device_props().smem_optin - fixed;
+  const int nk = (K + KC - 1) / KC;
+  int stages = std::min(std::max(2 * nk, 4), std::min(8, budget / stage_bytes));
   if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pw: not enough shared memory for 2 stages");
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  const size_t smem = (size_t)fixed + (size_t)stages * stage_bytes;
   auto kern = pw_tc_kernel<DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int total = ((M + 127) / 128) * nbn;
   const int grid = std::min(total, device_props().sms);
-  kern<<<grid, 192, smem, st>>>(ta, tb, ep, static_cast<uint8_t*>(y), M, N, K, BN, nbn, stages, pow2_cols(2 * BN));
+  kern<<<grid, 320, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, stages, pow2_cols(2 * BN), ncap);
   return check_launch("pw_tc_kernel");
 }
 
@@ -585,16 +653,15 @@ int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, 
 
 template <int DT, int K, int S>
 static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const void* wp, const Epi& ep, void* y,
-                         const Geo& g, int nsplit, cudaStream_t st) {
+                         const Geo& g, int nsplit_req, cudaStream_t st) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   const int th_in = (g.th - 1) * S + K, tw_in = (g.tw - 1) * S + K;
   if (g.nb * g.th * g.tw > 128) return set_error(FCM_E_INFEASIBLE, "dwpw: tile has more than 128 pixels");
   if (th_in > 256 || tw_in > 256 || g.nb > 256) return set_error(FCM_E_INFEASIBLE, "dwpw: halo box > 256");
-  if (nsplit <= 0) nsplit = (g.Cout + 255) / 256;
-  const int BN = round_up((g.Cout + nsplit - 1) / nsplit, 16);
-  if (BN > 256) return set_error(FCM_E_INFEASIBLE, "dwpw: C_out slice > 256 (raise n_split)");
-  CUtensorMap tx, tb;
+  int nsplit = 0;
+  const int BN = pick_bn<DT>(g.Cout, nsplit_req, nsplit);
+  CUtensorMap tx, tb, ty;
   {
     const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
     const uint64_t str[3] = {(uint64_t)g.C * ES, (uint64_t)g.W * g.C * ES, (uint64_t)g.H * g.W * g.C * ES};
@@ -609,22 +676,31 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
     if (!encode_tmap(&tb, tmap_dtype(DT), 2, wp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return set_error(FCM_E_CUDA, "tensor map (DWPW B) failed");
   }
+  {
+    const uint64_t dims[4] = {(uint64_t)g.Cout, (uint64_t)g.Wo, (uint64_t)g.Ho, (uint64_t)g.N};
+    const uint64_t str[3] = {(uint64_t)g.Cout * ES, (uint64_t)g.Wo * g.Cout * ES, (uint64_t)g.Ho * g.Wo * g.Cout * ES};
+    const uint32_t box[4] = {(uint32_t)(128 / ES), (uint32_t)g.tw, (uint32_t)g.th, (uint32_t)g.nb};
+    if (!encode_tmap(&ty, tmap_dtype(DT), 4, y, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return set_error(FCM_E_CUDA, "tensor map (DWPW Y) failed");
+  }
+  const int ncap = round_up(nsplit * BN, 16);
+  const int nk = (g.C + KC - 1) / KC;
+  const int fixed = 1024 + 32768 + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + K * K * nk * 128 + 256;
   const int xbytes = g.nb * th_in * tw_in * 128;
   const int stage_bytes = ((xbytes + 1023) & ~1023) + 16384 + BN * 128;
-  const int budget = device_props().smem_optin - 2048;
+  const int budget = device_props().smem_optin - fixed;
   const int stages = std::min(4, budget / stage_bytes);
   if (stages < 2) return set_error(FCM_E_INFEASIBLE, "dwpw: tile too large for 2 smem stages");
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (3 * stages + 4) * 8 + 16;
+  const size_t smem = (size_t)fixed + (size_t)stages * stage_bytes;
   auto kern = dwpw_tc_kernel<DT, K, S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
   const int grid = std::min(total, device_props().sms);
   using TT = typename Tr<DT>::T;
-  kern<<<grid, (4 + kDwpwNDW + 2) * 32, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ed, ep,
-                                                     static_cast<uint8_t*>(y), g.N, g.C, g.Ho, g.Wo, g.Cout, g.pt,
-                                                     g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, nsplit, BN, stages,
-                                                     pow2_cols(2 * BN));
+  kern<<<grid, (4 + kDwpwNDW + 2) * 32, smem, st>>>(tx, tb, ty, static_cast<const TT*>(wdw), ed, ep, g.N, g.C, g.Ho,
+                                                     g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y,
+                                                     nsplit, BN, stages, pow2_cols(2 * BN), ncap);
   return check_launch("dwpw_tc_kernel");
 }
 
@@ -675,19 +751,23 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   }
   const int stage_bytes = MB * 16384 + TD * 128;
   const int tbytes = ((R * (128 + 16)) + 1023) & ~1023;
-  const int budget = device_props().smem_optin - 2048 - 2 * tbytes;
+  const int ncap = round_up(g.Cout, TD);
+  const int nslice = ncap / TD;
+  const int fixed = 1024 + 2 * tbytes + 2 * consts_bytes<DT>(ncap) + K * K * nslice * 128 + 256;
+  const int budget = device_props().smem_optin - fixed;
   const int stages = std::min(4, budget / stage_bytes);
   if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pwdw_r: tile too large for 2 smem stages");
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + 2 * tbytes + (2 * stages + 4) * 8 + 16;
+  const size_t smem = (size_t)fixed + (size_t)stages * stage_bytes;
   auto kern = pwdw_tc_kernel<DT, K, S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
-  const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * ((g.Cout + TD - 1) / TD);
+  const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nslice;
   const int grid = std::min(total, device_props().sms);
   using TT = typename Tr<DT>::T;
-  kern<<<grid, 320, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ep, ed, static_cast<uint8_t*>(y), g.N, g.H, g.W,
-                                g.C, g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages,
-                                pow2_cols(2 * MB * TD));
+  kern<<<grid, (4 + kPwdwNDW + 2) * 32, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ep, ed,
+                                                     static_cast<uint8_t*>(y), g.N, g.H, g.W, g.C, g.Ho, g.Wo, g.Cout,
+                                                     g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages,
+                                                     pow2_cols(2 * MB * TD), ncap);
   return check_launch("pwdw_tc_kernel");
 }
 

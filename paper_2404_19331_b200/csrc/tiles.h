@@ -9,6 +9,17 @@ namespace fcm {
 
 inline int halo(int t, int k, int s) { return (t - 1) * s + k; }
 
+// Column block width of the tensor-core PW stage: one block when N <= 256 (padded to the MMA
+// granule of 16; the TMA store clips the tail), otherwise a multiple of the 128-byte store chunk
+// (cpc columns) so that blocks never overlap. nb_out = number of blocks.
+inline int pick_bn(int N, int nsplit, int cpc, int& nb_out) {
+  if (nsplit <= 0) nsplit = (N + 255) / 256;
+  int bn = (nsplit == 1) ? (N + 15) / 16 * 16 : ((N + nsplit - 1) / nsplit + cpc - 1) / cpc * cpc;
+  bn = std::min(bn, 256);
+  nb_out = (N + bn - 1) / bn;
+  return bn;
+}
+
 // LBL DW: one 128-byte channel group x th x tw outputs per CTA.
 inline void default_dw_tile(Geo& g) {
   g.th = std::min(g.s == 1 ? 8 : 4, g.Ho);

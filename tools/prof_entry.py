@@ -1,0 +1,27 @@
+"""Run selected plan entries of a network (for ncu captures): python tools/prof_entry.py --entries 0,3"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2404_19331_b200 as fcm  # noqa: E402
+from paper_2404_19331_b200.network import Network, model_json  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--net", default="mobilenet_v2")
+ap.add_argument("--dtype", default="bf16")
+ap.add_argument("--batch", type=int, default=256)
+ap.add_argument("--entries", default="0")
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+plan = fcm.plan(model_json(a.net, a.dtype, a.batch))
+netw = Network(a.net, a.dtype, a.batch, plan)
+torch.cuda.synchronize()
+ids = list(range(len(netw.steps))) if a.entries == "all" else [int(i) for i in a.entries.split(",")]
+for i in ids:
+    for _ in range(a.reps):
+        netw.steps[i]()
+    torch.cuda.synchronize()
+    print(i, netw.step_info[i]["op"], netw.step_info[i]["layers"], netw.step_info[i]["tile"])
