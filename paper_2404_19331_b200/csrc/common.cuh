@@ -254,6 +254,99 @@ __device__ __forceinline__ void dw_segment(uint32_t src, int col_bytes, int row_
   }
 }
 
+// ---------------------------------------------------------------------------- paired-FP32 DW core
+// bf16 / fp16 with K = 3: a lane's 32-bit word holds 2 channels, kept as an fp32 pair in a 64-bit
+// register and accumulated with the sm_100 packed FFMA2 (fma.rn.f32x2: two IEEE fp32 FMAs per
+// instruction, identical results to two FFMAs). A segment of SEG output rows is fully unrolled:
+// no window-shift moves, SEG x 1 independent accumulation chains.
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+template <int DT>
+__device__ __forceinline__ uint64_t word_to_f2(uint32_t w) {
+  if constexpr (DT == FCM_BF16) {
+    return f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  } else {
+    __half2 h = *reinterpret_cast<__half2*>(&w);
+    float2 f = __half22float2(h);
+    return f2_pack(f.x, f.y);
+  }
+}
+
+template <int DT, int K>
+struct DwW2 {
+  uint64_t w[K][K];
+};
+
+template <int DT, int K>
+__device__ __forceinline__ void load_dw_weights2_smem(DwW2<DT, K>& W, const uint32_t* wsm, int cwords, int cw) {
+  const uint32_t a = smem_u32(wsm) + 4 * cw;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) W.w[i][j] = word_to_f2<DT>(lds32(a + 4 * (i * K + j) * cwords));
+}
+
+template <int DT, int K>
+__device__ __forceinline__ void load_dw_weights2(DwW2<DT, K>& W, const void* wdw, int C, int c) {
+  const uint32_t* g = static_cast<const uint32_t*>(wdw);
+  const int cw = c / 2;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) W.w[i][j] = (c < C) ? word_to_f2<DT>(__ldg(g + (i * K + j) * (C / 2) + cw)) : 0ull;
+}
+
+// Output rows y0 .. y0+SEG-1 (all computed; input rows clamped to max_row); sink(r, acc) gets the
+// compile-time row offset r and the fp32 pair accumulator.
+template <int DT, int K, int S, int SEG, class Sink>
+__device__ __forceinline__ void dw_seg2(uint32_t src, int col_bytes, int row_bytes, int y0, int max_row,
+                                        const DwW2<DT, K>& W, Sink&& sink) {
+  constexpr int WR = (SEG - 1) * S + K;
+  uint64_t win[WR][K];
+#pragma unroll
+  for (int i = 0; i < WR; ++i) {
+    const uint32_t rp = src + min(y0 * S + i, max_row) * row_bytes;
+#pragma unroll
+    for (int j = 0; j < K; ++j) win[i][j] = word_to_f2<DT>(lds32(rp + j * col_bytes));
+  }
+#pragma unroll
+  for (int r = 0; r < SEG; ++r) {
+    uint64_t acc = 0ull;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc = f2_fma(win[r * S + i][j], W.w[i][j], acc);
+    sink(r, acc);
+  }
+}
+
+// Epilogue of an fp32 pair -> packed bf16x2 / f16x2 word (scale/bias as pairs, clamp = activation).
+template <int DT>
+__device__ __forceinline__ uint32_t epi2_pack(uint64_t acc, uint64_t sc, uint64_t bi, float lo_c, float hi_c) {
+  float a, b;
+  f2_unpack(f2_fma(acc, sc, bi), a, b);
+  a = fminf(fmaxf(a, lo_c), hi_c);
+  b = fminf(fmaxf(b, lo_c), hi_c);
+  if constexpr (DT == FCM_BF16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
 // Load this lane's DW weights from a shared-memory copy of Wdw laid out [k*k][C/VEC words].
 template <int DT, int K>
 __device__ __forceinline__ void load_dw_weights_smem(DwW<DT, K>& W, const uint32_t* wsm, int cwords, int cw) {

@@ -40,26 +40,54 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     tma_load_4d(xs, &tmx, &bar, c0, tx * tw * S - pl, ty * th * S - pt, n);
   }
   const int c = c0 + lane * V;
-  DwW<DT, K> W;
-  load_dw_weights<DT, K>(W, wdw, C, c);
-  EpiC ec[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ep, c + v, c + v < C);
-  mbar_wait(&bar, 0);
   const int y0 = ty * th, x0 = tx * tw;
   const int nrows = min(th, Ho - y0);
   uint32_t* yw = reinterpret_cast<uint32_t*>(y);
-  for (int col = warp; col < tw; col += 4) {
-    const int x = x0 + col;
-    if (x >= Wo) break;
-    const uint32_t src = smem_u32(xs) + ((col * S) * 32 + lane) * 4;
-    dw_segment<DT, K, S>(src, 128, tw_in * 128, 0, nrows, th_in - 1, W,
-                         [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
-                           if (c < C) {
-                             const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
-                             yw[(pix * C + c) / V] = epi_pack<DT>(acc, ec, ep);
-                           }
-                         });
+  constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
+  if constexpr (kPair) {
+    // same paired-FP32 core and segment length as the fused kernels (bit-identical DW)
+    constexpr int kSeg = (S == 1) ? 4 : 2;
+    DwW2<DT, K> W2;
+    load_dw_weights2<DT, K>(W2, wdw, C, c);
+    const bool cval = c < C;
+    const uint64_t sc2 = f2_pack(cval ? (ep.scale ? ep.scale[c] : 1.f) : 0.f, cval ? (ep.scale ? ep.scale[c + 1] : 1.f) : 0.f);
+    const uint64_t bi2 = f2_pack(cval && ep.bias ? ep.bias[c] : 0.f, cval && ep.bias ? ep.bias[c + 1] : 0.f);
+    const float lo_c = act_lo(ep.act), hi_c = act_hi(ep.act);
+    mbar_wait(&bar, 0);
+    const int nseg = (nrows + kSeg - 1) / kSeg;
+    for (int item = warp; item < tw * nseg; item += 4) {
+      const int col = item / nseg, seg = item - col * nseg;
+      const int x = x0 + col;
+      if (x >= Wo) continue;
+      const int ys = seg * kSeg;
+      const uint32_t src = smem_u32(xs) + ((col * S) * 32 + lane) * 4;
+      uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + x) * C + c) / V;
+      const size_t rstride = (size_t)Wo * C / V;
+      const int nvalid = nrows - ys;
+      dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
+        if (r < nvalid && cval) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
+      });
+    }
+    return;
+  } else {
+    DwW<DT, K> W;
+    load_dw_weights<DT, K>(W, wdw, C, c);
+    EpiC ec[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ep, c + v, c + v < C);
+    mbar_wait(&bar, 0);
+    for (int col = warp; col < tw; col += 4) {
+      const int x = x0 + col;
+      if (x >= Wo) break;
+      const uint32_t src = smem_u32(xs) + ((col * S) * 32 + lane) * 4;
+      dw_segment<DT, K, S>(src, 128, tw_in * 128, 0, nrows, th_in - 1, W,
+                           [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
+                             if (c < C) {
+                               const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
+                               yw[(pix * C + c) / V] = epi_pack<DT>(acc, ec, ep);
+                             }
+                           });
+    }
   }
 }
 

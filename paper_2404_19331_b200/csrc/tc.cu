@@ -11,6 +11,7 @@
 // Accumulators live in TMEM, double-buffered so the epilogue of tile i overlaps tile i+1.
 // One 32-bit word of channels per lane; a K chunk is one 128-byte row (64 bf16 / 128 int8).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "host.h"
@@ -214,50 +215,55 @@ __global__ void __launch_bounds__(320, 1)
 // the MMA) x one C_out slice of BN channels; the C_in (=K) dimension streams through in
 // 128-byte chunks, so the intermediate "contains all channels" in time, not space.
 // =====================================================================================
-constexpr int kDwpwNDW = 8;
+// DW warps per DWPW CTA: 16 for the paired-FP32 bf16/f16 3x3 core (fits 93 registers), else 8.
+template <int DT, int K> constexpr int dwpw_ndw() { return ((DT == FCM_BF16 || DT == FCM_F16) && K == 3) ? 16 : 8; }
+constexpr int kDwpwNA = 2;  // A-operand (commBuffer) ring depth
 
 template <int DT, int K, int S>
-__global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
+__global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
     dwpw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                    const __grid_constant__ CUtensorMap tmy, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
                    Epi ep, int N, int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw,
-                   int tiles_x, int tiles_y, int nsplit, int BN, int stages, uint32_t tmem_cols, int ncap) {
+                   int tiles_x, int tiles_y, int nsplit, int BN, int XS, int BS, uint32_t tmem_cols, int ncap, int dbg) {
   constexpr int V = Tr<DT>::VEC;
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
-  constexpr int WARP_TMA = 4 + kDwpwNDW, WARP_MMA = 5 + kDwpwNDW;
+  constexpr int kDwpwNDW = dwpw_ndw<DT, K>();
+  constexpr int WARP_TX = 4 + kDwpwNDW, WARP_TB = 5 + kDwpwNDW, WARP_MMA = 6 + kDwpwNDW;
   const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
   const int xbytes = nb * th_in * tw_in * 128;
   const int xstride = (xbytes + 1023) & ~1023;
-  const int stage_bytes = xstride + 16384 + BN * 128;
+  const int nk = (Cin + KC - 1) / KC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* ostage = smem;                          // 2 x 16 KB output staging
-  uint8_t* sbase = smem + 32768;
-  const int nk = (Cin + KC - 1) / KC;
-  uint8_t* cst = sbase + stages * stage_bytes;
+  uint8_t* ostage = smem;                        // 2 x 16 KB output staging
+  uint8_t* abuf = smem + 32768;                  // kDwpwNA x 16 KB A operand (commBuffer) ring
+  uint8_t* xbuf = abuf + kDwpwNA * 16384;        // XS x X halo chunks (TMA -> DW)
+  uint8_t* bbuf = xbuf + XS * xstride;           // BS x PW weight chunks (TMA -> MMA)
+  uint8_t* cst = bbuf + BS * BN * 128;
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(nk * KC));  // DW weights
-  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + K * K * nk * 32);
-  uint64_t* afull = full + stages;
-  uint64_t* empty = afull + stages;
-  uint64_t* tfull = empty + stages;
+  uint64_t* fullX = reinterpret_cast<uint64_t*>(wsm + K * K * nk * 32);
+  uint64_t* emptyX = fullX + XS;
+  uint64_t* fullB = emptyX + XS;
+  uint64_t* emptyB = fullB + BS;
+  uint64_t* afull = emptyB + BS;
+  uint64_t* aempty = afull + kDwpwNA;
+  uint64_t* tfull = aempty + kDwpwNA;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cout, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cin, nk * KC, dcst);
   stage_dw_weights<DT>(wdw, K, Cin, nk * 32, wsm);
-  if (warp == WARP_TMA && lane == 0) {
+  if (warp == WARP_TX && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
     tma_prefetch_desc(&tmy);
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(afull + s, kDwpwNDW * 32);
-      mbar_init(empty + s, 1);
-    }
+    for (int s = 0; s < XS; ++s) { mbar_init(fullX + s, 1); mbar_init(emptyX + s, kDwpwNDW); }
+    for (int s = 0; s < BS; ++s) { mbar_init(fullB + s, 1); mbar_init(emptyB + s, 1); }
+    for (int a = 0; a < kDwpwNA; ++a) { mbar_init(afull + a, kDwpwNDW * 32); mbar_init(aempty + a, 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 128); }
     fence_barrier_init();
   }
@@ -277,20 +283,30 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
     nbi = sp / tiles_y;
   };
 
-  if (warp == WARP_TMA) {
+  if (warp == WARP_TX) {
     if (lane == 0) {
-      const uint32_t tx = xbytes + BN * 128;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int ns, nbi, tyi, txi;
         decode(t, ns, nbi, tyi, txi);
         for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % stages;
-          mbar_wait(empty + s, ((it / stages) & 1) ^ 1);
-          uint8_t* st = sbase + s * stage_bytes;
-          mbar_arrive_expect_tx(full + s, tx);
-          tma_load_4d(st, &tmx, full + s, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
-          tma_load_2d(st + xstride + 16384, &tmb, full + s, kc * KC, ns * BN);
+          const int s = it % XS;
+          mbar_wait(emptyX + s, ((it / XS) & 1) ^ 1);
+          mbar_arrive_expect_tx(fullX + s, xbytes);
+          tma_load_4d(xbuf + s * xstride, &tmx, fullX + s, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
+        }
+      }
+    }
+  } else if (warp == WARP_TB) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int ns = t % nsplit;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % BS;
+          mbar_wait(emptyB + s, ((it / BS) & 1) ^ 1);
+          mbar_arrive_expect_tx(fullB + s, BN * 128);
+          tma_load_2d(bbuf + s * BN * 128, &tmb, fullB + s, kc * KC, ns * BN);
         }
       }
     }
@@ -304,17 +320,16 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
         tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          mbar_wait(full + s, ph);
-          mbar_wait(afull + s, ph);
+          const int a = it % kDwpwNA, sb = it % BS;
+          mbar_wait(afull + a, (it / kDwpwNA) & 1);
+          mbar_wait(fullB + sb, (it / BS) & 1);
           tc_fence_after();
-          uint8_t* st = sbase + s * stage_bytes;
-          const uint64_t ad = smem_desc_sw128(smem_u32(st + xstride));
-          const uint64_t bd = smem_desc_sw128(smem_u32(st + xstride + 16384));
+          const uint64_t ad = smem_desc_sw128(smem_u32(abuf + a * 16384));
+          const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + sb * BN * 128));
 #pragma unroll
           for (int k = 0; k < 4; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
-          mma_commit(empty + s);
+          mma_commit(aempty + a);
+          mma_commit(emptyB + sb);
         }
         mma_commit(tfull + acc);
       }
@@ -322,37 +337,65 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
   } else if (warp >= 4) {
     // ---------------- DW warps: X halo chunk (smem) -> DW -> eps_dw -> A operand (commBuffer)
     // work item = (output column, segment of kSeg rows), round-robin over the DW warps
-    constexpr int kSeg = 8;
+    constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
+    constexpr int kSeg = kPair ? (S == 1 ? 4 : 2) : 8;
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       for (int kc = 0; kc < nk; ++kc, ++it) {
-        const int s = it % stages;
+        const int sx = it % XS, a = it % kDwpwNA;
         const int c = kc * KC + lane * V;
-        DwW<DT, K> W;
-        load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + lane);
-        EpiC ec[V];
+        const uint32_t st = smem_u32(xbuf + sx * xstride);
+        const uint32_t abase = smem_u32(abuf + a * 16384);
+        if constexpr (kPair) {
+          DwW2<DT, K> W2;
+          load_dw_weights2_smem<DT, K>(W2, wsm, nk * 32, kc * 32 + lane);
+          const uint64_t sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1)), bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
+          const bool cval = c < Cin;
+          const float lo_c = act_lo(ed.act), hi_c = act_hi(ed.act);
+          mbar_wait(fullX + sx, (it / XS) & 1);
+          mbar_wait(aempty + a, ((it / kDwpwNA) & 1) ^ 1);
+          for (int item = dw; item < nitems && !(dbg & 1); item += kDwpwNDW) {
+            const int col = item / nseg, seg = item - col * nseg;
+            const int b = col / tw, x = col - b * tw;
+            const int y0 = seg * kSeg;
+            const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
+            const int mbase = (b * th + y0) * tw + x;
+            const int nvalid = th - y0;
+            dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+              if (r < nvalid) {
+                const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
+                sts32(abase + sw128_off(mbase + r * tw, lane), word);
+              }
+            });
+          }
+        } else {
+          DwW<DT, K> W;
+          load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + lane);
+          EpiC ec[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
-        mbar_wait(full + s, (it / stages) & 1);
-        const uint32_t st = smem_u32(sbase + s * stage_bytes);
-        const uint32_t abase = st + xstride;
-        for (int item = dw; item < nitems; item += kDwpwNDW) {
-          const int col = item / nseg, seg = item - col * nseg;
-          const int b = col / tw, x = col - b * tw;
-          const int y0 = seg * kSeg;
-          const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
-          dw_segment<DT, K, S>(src, 128, tw_in * 128, y0, min(kSeg, th - y0), th_in - 1, W,
-                               [&](int yy, const typename Tr<DT>::acc_t(&a)[V]) {
-                                 const int m = (b * th + yy) * tw + x;
-                                 const uint32_t word = (c < Cin) ? epi_pack<DT>(a, ec, ed) : 0u;
-                                 sts32(abase + sw128_off(m, lane), word);
-                               });
+          for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
+          mbar_wait(fullX + sx, (it / XS) & 1);
+          mbar_wait(aempty + a, ((it / kDwpwNA) & 1) ^ 1);
+          for (int item = dw; item < nitems; item += kDwpwNDW) {
+            const int col = item / nseg, seg = item - col * nseg;
+            const int b = col / tw, x = col - b * tw;
+            const int y0 = seg * kSeg;
+            const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
+            dw_segment<DT, K, S>(src, 128, tw_in * 128, y0, min(kSeg, th - y0), th_in - 1, W,
+                                 [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
+                                   const int m = (b * th + yy) * tw + x;
+                                   const uint32_t word = (c < Cin) ? epi_pack<DT>(acc, ec, ed) : 0u;
+                                   sts32(abase + sw128_off(m, lane), word);
+                                 });
+          }
         }
         fence_proxy_async_smem();
-        mbar_arrive(afull + s);
+        mbar_arrive(afull + a);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(emptyX + sx);
       }
     }
   } else {
@@ -364,8 +407,9 @@ __global__ void __launch_bounds__((4 + kDwpwNDW + 2) * 32, 1)
       decode(t, ns, nbi, tyi, txi);
       mbar_wait(tfull + acc, (local >> 1) & 1);
       tc_fence_after();
-      epilogue_tile<DT, 4>(tbase + acc * BN, BN, ns * BN, Cout, cs, ep, ostage, sbuf,
-                           [&](const uint8_t* buf, int c) { tma_store_4d(&tmy, buf, c, txi * tw, tyi * th, nbi * nb); });
+      if (!(dbg & 2))
+        epilogue_tile<DT, 4>(tbase + acc * BN, BN, ns * BN, Cout, cs, ep, ostage, sbuf,
+                             [&](const uint8_t* buf, int c) { tma_store_4d(&tmy, buf, c, txi * tw, tyi * th, nbi * nb); });
       tc_fence_before();
       mbar_arrive(tempty + acc);
     }
@@ -538,10 +582,12 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
     }
   } else {
     // ---------------- DW consumers: T tile -> DW -> eps_dw -> OFM (128 B per warp store)
-    constexpr int kSeg = 8;
+    constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
+    constexpr int kSeg = kPair ? (S == 1 ? 8 : 4) : 8;
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
+    const float lo_c = act_lo(ed.act), hi_c = act_hi(ed.act);
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -549,29 +595,51 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       const int c = sl * TD + lane * V;
-      DwW<DT, K> Wd;
-      load_dw_weights_smem<DT, K>(Wd, wsm, nslice * 32, sl * 32 + lane);
-      EpiC ec[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
-      mbar_wait(Tfull + tbi, (local >> 1) & 1);
       const uint32_t tsa = smem_u32(tsm + tbi * tbytes);
       const int y0t = tyi * th;
       const int nrows_t = min(th, Ho - y0t);
-      for (int item = dw; item < nitems; item += kPwdwNDW) {
-        const int col = item / nseg, seg = item - col * nseg;
-        const int b = col / tw, x = col - b * tw;
-        const int n = nbi * nb + b, xo = txi * tw + x;
-        const int y0 = seg * kSeg;
-        if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
-        const uint32_t src = tsa + (((b * th_in) * tw_in + x * S) * PW + lane) * 4;
-        dw_segment<DT, K, S>(src, PITCH, tw_in * PITCH, y0, min(kSeg, nrows_t - y0), th_in - 1, Wd,
-                             [&](int yy, const typename Tr<DT>::acc_t(&a)[V]) {
-                               if (c < Cmid) {
-                                 const size_t pix = ((size_t)n * Ho + (y0t + yy)) * Wo + xo;
-                                 yw[(pix * Cmid + c) / V] = epi_pack<DT>(a, ec, ed);
-                               }
-                             });
+      if constexpr (kPair) {
+        DwW2<DT, K> W2;
+        load_dw_weights2_smem<DT, K>(W2, wsm, nslice * 32, sl * 32 + lane);
+        const uint64_t sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1)), bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
+        const bool cval = c < Cmid;
+        mbar_wait(Tfull + tbi, (local >> 1) & 1);
+        for (int item = dw; item < nitems; item += kPwdwNDW) {
+          const int col = item / nseg, seg = item - col * nseg;
+          const int b = col / tw, x = col - b * tw;
+          const int n = nbi * nb + b, xo = txi * tw + x;
+          const int y0 = seg * kSeg;
+          if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
+          const uint32_t src = tsa + (((b * th_in) * tw_in + x * S) * PW + lane) * 4;
+          const int nvalid = nrows_t - y0;
+          uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
+          const size_t rstride = (size_t)Wo * Cmid / V;
+          dw_seg2<DT, K, S, kSeg>(src, PITCH, tw_in * PITCH, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+            if (r < nvalid && cval) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
+          });
+        }
+      } else {
+        DwW<DT, K> Wd;
+        load_dw_weights_smem<DT, K>(Wd, wsm, nslice * 32, sl * 32 + lane);
+        EpiC ec[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
+        mbar_wait(Tfull + tbi, (local >> 1) & 1);
+        for (int item = dw; item < nitems; item += kPwdwNDW) {
+          const int col = item / nseg, seg = item - col * nseg;
+          const int b = col / tw, x = col - b * tw;
+          const int n = nbi * nb + b, xo = txi * tw + x;
+          const int y0 = seg * kSeg;
+          if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
+          const uint32_t src = tsa + (((b * th_in) * tw_in + x * S) * PW + lane) * 4;
+          dw_segment<DT, K, S>(src, PITCH, tw_in * PITCH, y0, min(kSeg, nrows_t - y0), th_in - 1, Wd,
+                               [&](int yy, const typename Tr<DT>::acc_t(&a)[V]) {
+                                 if (c < Cmid) {
+                                   const size_t pix = ((size_t)n * Ho + (y0t + yy)) * Wo + xo;
+                                   yw[(pix * Cmid + c) / V] = epi_pack<DT>(a, ec, ed);
+                                 }
+                               });
+        }
       }
       mbar_arrive(Tempty + tbi);
     }
@@ -584,6 +652,13 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
 }
 
 // ------------------------------------------------------------------------------- launchers
+// FCM_DEBUG_FLAGS (env, development only): bit 0 skip DW math, bit 1 skip PW epilogue, bit 2 DW
+// warps do not wait for the TMA. Results are wrong when set; used to attribute time to roles.
+static int debug_flags() {
+  static int f = [] { const char* e = getenv("FCM_DEBUG_FLAGS"); return e ? atoi(e) : 0; }();
+  return f;
+}
+
 static uint32_t pow2_cols(uint32_t c) {
   uint32_t r = 32;
   while (r < c) r <<= 1;
@@ -685,22 +760,23 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   }
   const int ncap = round_up(nsplit * BN, 16);
   const int nk = (g.C + KC - 1) / KC;
-  const int fixed = 1024 + 32768 + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + K * K * nk * 128 + 256;
-  const int xbytes = g.nb * th_in * tw_in * 128;
-  const int stage_bytes = ((xbytes + 1023) & ~1023) + 16384 + BN * 128;
-  const int budget = device_props().smem_optin - fixed;
-  const int stages = std::min(4, budget / stage_bytes);
-  if (stages < 2) return set_error(FCM_E_INFEASIBLE, "dwpw: tile too large for 2 smem stages");
-  const size_t smem = (size_t)fixed + (size_t)stages * stage_bytes;
+  const int fixed = 1024 + 32768 + kDwpwNA * 16384 + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + K * K * nk * 128 + 512;
+  const int xstride = ((g.nb * th_in * tw_in * 128) + 1023) & ~1023;
+  const int BS = 2;
+  const int budget = device_props().smem_optin - fixed - BS * BN * 128;
+  const int XS = std::min(6, budget / xstride);
+  if (XS < 2) return set_error(FCM_E_INFEASIBLE, "dwpw: tile too large for 2 X stages");
+  const size_t smem = (size_t)fixed + (size_t)BS * BN * 128 + (size_t)XS * xstride;
   auto kern = dwpw_tc_kernel<DT, K, S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
   const int grid = std::min(total, device_props().sms);
   using TT = typename Tr<DT>::T;
-  kern<<<grid, (4 + kDwpwNDW + 2) * 32, smem, st>>>(tx, tb, ty, static_cast<const TT*>(wdw), ed, ep, g.N, g.C, g.Ho,
-                                                     g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y,
-                                                     nsplit, BN, stages, pow2_cols(2 * BN), ncap);
+  kern<<<grid, (4 + dwpw_ndw<DT, K>() + 3) * 32, smem, st>>>(tx, tb, ty, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
+                                                              g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw,
+                                                              tiles_x, tiles_y, nsplit, BN, XS, BS, pow2_cols(2 * BN),
+                                                              ncap, debug_flags());
   return check_launch("dwpw_tc_kernel");
 }
 
