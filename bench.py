@@ -267,10 +267,20 @@ def main():
         t = torch.tensor([t_ms, t_e2e], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_ms, t_e2e = float(t[0]), float(t[1])
-        # verification only (after timing): gather per-image checksums over NCCL
-        ck = netw.out.float().reshape(args.batch, -1).sum(1).double()
+        # verification only (after timing): gather per-image checksums over NCCL; rank 0
+        # recomputes the first images of every shard itself -- batch shards are independent,
+        # so the results must be bit-identical
+        ck = netw.out.double().reshape(args.batch, -1).sum(1)
         allck = [torch.empty_like(ck) for _ in range(ws)]
         torch.distributed.all_gather(allck, ck)
+        verify = {"gathered_images": ws * args.batch, "checked": 0, "bit_identical": True}
+        if rank == 0:
+            for r in range(ws):
+                probe = Network(args.net, args.dtype, 2, plan, device=dev, n0=r * args.batch)
+                probe.run()
+                mine = probe.out.double().reshape(2, -1).sum(1)
+                verify["checked"] += 2
+                verify["bit_identical"] &= bool(torch.equal(mine, allck[r][:2]))
 
     pk = peaks()
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
@@ -322,6 +332,8 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
         }
+        if ws > 1:
+            line["verify"] = verify
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = cpu_baseline(args.net, args.dtype, args.cpu_seconds)
         if args.layers_out:
