@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layers-out", default="", help="write the per-entry table (JSON) here")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly (for ncu launch lists)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -209,7 +210,17 @@ def main():
 
     plan = fcm.plan(model_json(args.net, args.dtype, args.batch, args.mode))
     netw = Network(args.net, args.dtype, args.batch, plan, device=dev, n0=rank * args.batch)
-    graph = netw.capture()
+    if args.no_graph:
+        netw.run()
+        torch.cuda.synchronize()
+
+        class _Eager:
+            @staticmethod
+            def replay():
+                netw.run()
+        graph = _Eager()
+    else:
+        graph = netw.capture()
     launches_per_step = len(netw.steps)
     st = torch.cuda.current_stream()
 

@@ -1,0 +1,15 @@
+"""Small-shape run of every kernel family for compute-sanitizer (memcheck/racecheck/synccheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from tests.cases import Case  # noqa: E402
+
+for args, kw in [(("dw", "bf16", 1, 9, 11, 64), {}), (("dw", "s8", 1, 9, 7, 32), {"k": 5}),
+                 (("pw", "bf16", 1, 9, 11, 40, 24), {}), (("pw", "s8", 1, 5, 7, 32, 48), {}),
+                 (("dwpw", "bf16", 2, 9, 11, 96, 40), {}), (("dwpw", "s8", 1, 9, 9, 32, 48), {"k": 5, "s": 2}),
+                 (("pwdw", "bf16", 2, 9, 11, 24, 72), {}), (("pwdw", "bf16", 1, 12, 12, 24, 72), {"s": 2}),
+                 (("pwdw", "s8", 1, 9, 9, 32, 48), {}), (("dwpw", "f32", 1, 9, 9, 16, 32), {}),
+                 (("pwdw", "f32", 1, 9, 9, 16, 32), {})]:
+    Case(*args, **kw).check()
+    print("ok", args, kw, flush=True)
