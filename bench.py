@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--batch", type=int, default=256, help="images per GPU")
     ap.add_argument("--mode", default="b200", choices=["b200", "paper"])
+    ap.add_argument("--plan", default="measured", choices=["measured", "model"],
+                    help="measured: refine the planner's choice with timed candidates (autotune.refine)")
+    ap.add_argument("--plan-out", default="", help="write the executed plan (JSON) here")
     ap.add_argument("--ref-images", type=int, default=1, help="reference arm: images per step")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -208,7 +211,14 @@ def main():
     import paper_2404_19331_b200 as fcm
     from paper_2404_19331_b200.network import Network, model_json
 
-    plan = fcm.plan(model_json(args.net, args.dtype, args.batch, args.mode))
+    if args.plan == "measured" and args.mode == "b200":
+        from paper_2404_19331_b200.autotune import refine
+        plan = refine(args.net, args.dtype, args.batch, device=dev)
+    else:
+        plan = fcm.plan(model_json(args.net, args.dtype, args.batch, args.mode))
+    if args.plan_out and rank == 0:
+        with open(args.plan_out, "w") as f:
+            json.dump(plan, f, indent=1)
     netw = Network(args.net, args.dtype, args.batch, plan, device=dev, n0=rank * args.batch)
     if args.no_graph:
         netw.run()
@@ -325,7 +335,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded splitmix64 inputs/weights, random-init)",
             "config": {"workload": f"{args.net} DW/PW stack (configs[2]), {args.batch} img/GPU, 224x224",
-                       "net": args.net, "global_batch": ws * args.batch, "plan_mode": args.mode,
+                       "net": args.net, "global_batch": ws * args.batch, "plan_mode": plan["mode"],
                        "fused_pairs": plan["totals"]["fused_pairs"], "kernels_per_step": launches_per_step,
                        "parallelism": f"batch-sharded x{ws} (replicas, no collective on the hot path)",
                        "l2": "inputs larger than L2 (205 MB input + 2.8 GB compulsory traffic per step)",

@@ -197,6 +197,11 @@ def _bn(co, ns, b):
     return min((ceil(co / ns) + cpc - 1) // cpc * cpc, 256)
 
 
+def _simt(dtype, b, *chans):
+    """fp32 and any NHWC pitch that is not a multiple of 16 bytes run on the CUDA-core kernels."""
+    return dtype == "f32" or any((c * b) % 16 for c in chans)
+
+
 def b200_numbers(op, layers, N, dtype, tile):
     """Compulsory HBM bytes, exact L2->SM bytes and MACs of one candidate at its reported tile."""
     b = ESZ[dtype]
@@ -204,7 +209,7 @@ def b200_numbers(op, layers, N, dtype, tile):
     if op == "dw":
         d = layers[0]
         Ho, Wo = out_hw(d)
-        u = units("dw", N, d, d["c"], d["c"], 1, th, tw, 128 // b)
+        u = units("dw", N, d, d["c"], d["c"], 1, th, tw, d["c"] if (d["c"] * b) % 16 else 128 // b)
         dram = (N * (d["h"] * d["w"] * d["c"] + Ho * Wo * d["c"]) + d["k"] ** 2 * d["c"]) * b
         return dict(dram_bytes=dram, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
                     dw_macs=N * Ho * Wo * d["c"] * d["k"] ** 2, pw_macs=0, redundant_macs=0)
@@ -213,7 +218,7 @@ def b200_numbers(op, layers, N, dtype, tile):
         M = N * p["h"] * p["w"]
         ci, co = p["c_in"], p["c_out"]
         bm = th
-        bn = 64 if dtype == "f32" else _bn(co, ns, b)
+        bn = 64 if _simt(dtype, b, ci, co) else _bn(co, ns, b)
         u = pw_units(M, ci, co, bm, bn)
         return dict(dram_bytes=(M * (ci + co) + ci * co) * b, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
                     dw_macs=0, pw_macs=M * ci * co, redundant_macs=0)
@@ -221,7 +226,7 @@ def b200_numbers(op, layers, N, dtype, tile):
         d, p = layers
         Ho, Wo = out_hw(d)
         ci, co = d["c"], p["c_out"]
-        bn = 64 if dtype == "f32" else _bn(co, ns, b)
+        bn = 64 if _simt(dtype, b, ci, co) else _bn(co, ns, b)
         u = units("dwpw", N, d, ci, co, nb, th, tw, bn)
         dram = (N * (d["h"] * d["w"] * ci + Ho * Wo * co) + d["k"] ** 2 * ci + ci * co) * b
         return dict(dram_bytes=dram, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
@@ -229,7 +234,7 @@ def b200_numbers(op, layers, N, dtype, tile):
     p, d = layers
     Ho, Wo = out_hw(d)
     ci, cm = p["c_in"], p["c_out"]
-    td = 32 if dtype == "f32" else 128 // b
+    td = 32 if _simt(dtype, b, ci, cm) else 128 // b
     u = units("pwdw", N, d, ci, cm, nb, th, tw, td)
     dram = (N * (d["h"] * d["w"] * ci + Ho * Wo * cm) + ci * cm + d["k"] ** 2 * cm) * b
     return dict(dram_bytes=dram, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b, dw_macs=N * Ho * Wo * cm * d["k"] ** 2,

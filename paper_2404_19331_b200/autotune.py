@@ -1,0 +1,88 @@
+"""Measured plan refinement ("measure, don't guess").
+
+FusePlanner (fcm_plan, b200 mode) ranks options with an analytic time model. This module times
+every candidate the planner reports -- each layer's LBL kernel and each admissible FCM -- on the
+current GPU (CUDA events, L2-warm, the candidate's own tile) and re-runs the same decision rule
+(fuse iff strictly faster) and chain DP on the measured times.
+The returned plan has the planner's format; entries carry `measured_us`.
+"""
+from __future__ import annotations
+
+import copy
+
+import torch
+
+import paper_2404_19331_b200 as fcm
+from paper_2404_19331_b200.network import Network, model_json
+
+
+def _time(f, reps=10):
+    for _ in range(2):
+        f()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / reps
+
+
+def chain_dp(order, lbl, fcm_cost):
+    """Same DP as planner.cpp: dp over the layer chain, a fusion (i-1, i) wins exact ties."""
+    n = len(order)
+    dp, take = [0.0] * (n + 1), [0] * (n + 1)
+    for i in range(1, n + 1):
+        dp[i], take[i] = dp[i - 1] + lbl[order[i - 1]], 1
+        key = (order[i - 2], order[i - 1]) if i >= 2 else None
+        if key in fcm_cost and dp[i - 2] + fcm_cost[key] <= dp[i]:
+            dp[i], take[i] = dp[i - 2] + fcm_cost[key], 2
+    sel, i = [], n
+    while i > 0:
+        if take[i] == 2:
+            sel.append((order[i - 2], order[i - 1]))
+            i -= 2
+        else:
+            sel.append((order[i - 1],))
+            i -= 1
+    return sel[::-1], dp[n]
+
+
+def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=False):
+    plan = fcm.plan(model_json(net, dtype, batch))
+    cands = plan["candidates"]
+    # one Network instance whose "plan" is every candidate, so each has real buffers to run on
+    all_entries = [dict(c) for c in cands["lbl"]] + [dict(c) for c in cands["fcm"]]
+    probe = Network(net, dtype, batch, {"entries": []}, device=device)
+    order = probe.order
+    meas = {}
+    for c in all_entries:
+        lids = c["layers"]
+        l0 = probe.layers[lids[0]]
+        cin = l0["c"] if l0["kind"] == "dw" else l0["c_in"]
+        src = torch.zeros((batch, l0["h"], l0["w"], cin), dtype=probe.x.dtype, device=device)
+        out = torch.empty(probe._out_shape(lids[-1]), dtype=probe.x.dtype, device=device)
+        f = probe._make_call(c, src, out)
+        try:
+            meas[tuple(lids)] = _time(f, reps)
+        except Exception as e:  # infeasible tile etc.: never chosen
+            if verbose:
+                print("skip", lids, e)
+        del src, out
+    lbl = {l: meas[(l,)] for l in order}
+    fcm_cost = {k: v for k, v in meas.items() if len(k) == 2 and v < lbl[k[0]] + lbl[k[1]]}
+    sel, total = chain_dp(order, lbl, fcm_cost)
+    by_layers = {tuple(c["layers"]): c for c in all_entries}
+    entries = []
+    for s in sel:
+        e = copy.deepcopy(by_layers[s])
+        e["measured_us"] = meas[s]
+        entries.append(e)
+    out = dict(plan)
+    out["entries"] = entries
+    out["mode"] = "b200+measured"
+    out["totals"] = dict(plan["totals"], measured_us=total, dram_bytes=sum(e["dram_bytes"] for e in entries),
+                         fused_pairs=sum(1 for e in entries if len(e["layers"]) == 2))
+    out.pop("candidates", None)
+    return out

@@ -108,11 +108,7 @@ int check_tensor(const fcm_tensor* t, const char* name, bool allow_nchw) {
   return FCM_OK;
 }
 
-int check_pitch(const fcm_tensor* t, const char* name) {
-  if (t->layout == FCM_NHWC && ((size_t)t->c * elem_size(t->dtype)) % 16)
-    return set_error(FCM_E_ALIGN, std::string(name) + ": channel pitch C*elem must be a multiple of 16 bytes");
-  return FCM_OK;
-}
+bool pitch_ok(const fcm_tensor* t) { return ((size_t)t->c * elem_size(t->dtype)) % 16 == 0; }
 
 bool overlaps(const fcm_tensor* a, const fcm_tensor* b) {
   const char* a0 = static_cast<const char*>(a->data);
@@ -203,7 +199,8 @@ int fcm_dw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const
   Geo g{x->n, x->h, x->w, x->c, Ho, Wo, x->c, geom->k, geom->stride, geom->pad_t, geom->pad_l, 1, 0, 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (x->layout == FCM_NCHW) return launch_dw_nchw(x->dtype, x->data, w_dw, to_epi(ep), y->data, g, st);
-  FCM_TRY(check_pitch(x, "x"));
+  // channel pitch not a multiple of 16 B: TMA cannot address it -> CUDA-core kernel
+  if (!pitch_ok(x)) return launch_dw_simt(x->dtype, x->data, w_dw, to_epi(ep), y->data, g, st);
   default_dw_tile(g);
   if (tile) {
     if (tile->tile_h > 0) g.th = tile->tile_h;
@@ -224,11 +221,8 @@ int fcm_pw(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep,
   if (overlaps(x, y)) return set_error(FCM_E_INVAL, "pw: x and y overlap");
   const int M = x->n * x->h * x->w;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (x->dtype == FCM_F32)
-    return launch_pw_simt(static_cast<const float*>(x->data), static_cast<const float*>(w_pw_packed), to_epi(ep),
-                          static_cast<float*>(y->data), M, x->c, y->c, st);
-  FCM_TRY(check_pitch(x, "x"));
-  FCM_TRY(check_pitch(y, "y"));
+  if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y))
+    return launch_pw_simt(x->dtype, x->data, w_pw_packed, to_epi(ep), y->data, M, x->c, y->c, st);
   return launch_pw_tc(x->dtype, x->data, w_pw_packed, to_epi(ep), y->data, M, x->c, y->c, st);
 }
 
@@ -250,11 +244,8 @@ int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, con
   if (overlaps(x, y)) return set_error(FCM_E_INVAL, "dwpw: x and y overlap");
   Geo g{x->n, x->h, x->w, x->c, Ho, Wo, y->c, geom->k, geom->stride, geom->pad_t, geom->pad_l, 1, 0, 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (x->dtype == FCM_F32)
-    return launch_dwpw_simt(static_cast<const float*>(x->data), static_cast<const float*>(w_dw), to_epi(ep_dw),
-                            static_cast<const float*>(w_pw_packed), to_epi(ep_pw), static_cast<float*>(y->data), g, st);
-  FCM_TRY(check_pitch(x, "x"));
-  FCM_TRY(check_pitch(y, "y"));
+  if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y))
+    return launch_dwpw_simt(x->dtype, x->data, w_dw, to_epi(ep_dw), w_pw_packed, to_epi(ep_pw), y->data, g, st);
   int nsplit = 0;
   default_dwpw_tile(g);
   if (tile) {
@@ -284,11 +275,8 @@ int fcm_pwdw_r(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue*
   if (overlaps(x, y)) return set_error(FCM_E_INVAL, "pwdw_r: x and y overlap");
   Geo g{x->n, x->h, x->w, x->c, Ho, Wo, y->c, geom->k, geom->stride, geom->pad_t, geom->pad_l, 1, 0, 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (x->dtype == FCM_F32)
-    return launch_pwdw_simt(static_cast<const float*>(x->data), static_cast<const float*>(w_pw_packed), to_epi(ep_pw),
-                            static_cast<const float*>(w_dw), to_epi(ep_dw), static_cast<float*>(y->data), g, st);
-  FCM_TRY(check_pitch(x, "x"));
-  FCM_TRY(check_pitch(y, "y"));
+  if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y))
+    return launch_pwdw_simt(x->dtype, x->data, w_pw_packed, to_epi(ep_pw), w_dw, to_epi(ep_dw), y->data, g, st);
   default_pwdw_tile(g);
   if (tile) {
     if (tile->tile_h > 0) g.th = tile->tile_h;

@@ -41,14 +41,15 @@ struct Geo {
 // launchers (return FCM_OK or an FCM_E_* code; all validation already done by the API layer)
 int launch_dw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
 int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st);
-int launch_pw_simt(const float* x, const float* wp, const Epi& ep, float* y, int M, int K, int N, cudaStream_t st);
+int launch_pw_simt(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st);
+int launch_dw_simt(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
 int launch_dwpw_tc(int dt, const void* x, const void* wdw, const Epi& ed, const void* wp, const Epi& ep, void* y,
                    const Geo& g, int n_split, cudaStream_t st);
-int launch_dwpw_simt(const float* x, const float* wdw, const Epi& ed, const float* wp, const Epi& ep, float* y,
+int launch_dwpw_simt(int dt, const void* x, const void* wdw, const Epi& ed, const void* wp, const Epi& ep, void* y,
                      const Geo& g, cudaStream_t st);
 int launch_pwdw_tc(int dt, const void* x, const void* wp, const Epi& ep, const void* wdw, const Epi& ed, void* y,
                    const Geo& g, cudaStream_t st);
-int launch_pwdw_simt(const float* x, const float* wp, const Epi& ep, const float* wdw, const Epi& ed, float* y,
+int launch_pwdw_simt(int dt, const void* x, const void* wp, const Epi& ep, const void* wdw, const Epi& ed, void* y,
                      const Geo& g, cudaStream_t st);
 int launch_pack_pw(int dt, int cin, int cout, const void* w, void* packed, cudaStream_t st);
 int launch_dw_nchw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);

@@ -240,14 +240,19 @@ static Geo geo_of(const Layer& d, ll N, ll Cout) {
   return g;
 }
 
+// A 16-byte-misaligned NHWC channel pitch runs on the CUDA-core kernels (csrc/simt.cu), as does
+// fp32 for every PW-containing kernel.
+static bool aligned16(ll c, ll b) { return (c * b) % 16 == 0; }
+
 static Cost b200_dw(const Layer& d, ll N, int dt, ll b, const Gpu& gp) {
   Cost c;
   c.ok = true;
   c.op = "dw";
   Geo g = geo_of(d, N, d.C);
   default_dw_tile(g);
+  if (!aligned16(d.C, b)) { g.th = 1; g.tw = 1; }  // element-wise SIMT kernel: unit = one pixel
   c.th = g.th; c.tw = g.tw;
-  const Units u = units("dw", N, d, d.C, d.C, 1, g.th, g.tw, 128 / b);
+  const Units u = units("dw", N, d, d.C, d.C, 1, g.th, g.tw, aligned16(d.C, b) ? 128 / b : d.C);
   c.l2 = u.total() * b;
   c.dram = (N * (d.H * d.W * d.C + d.Ho * d.Wo * d.C) + d.k * d.k * d.C) * b;
   c.dw_macs = N * d.Ho * d.Wo * d.C * d.k * d.k;
@@ -261,7 +266,7 @@ static Cost b200_pw(const Layer& p, ll N, int dt, ll b, const Gpu& gp) {
   c.op = "pw";
   const ll M = N * p.H * p.W;
   ll bm = 128, bn;
-  if (dt == FCM_F32) {
+  if (dt == FCM_F32 || !aligned16(p.C, b) || !aligned16(p.Cout, b)) {
     bm = 64; bn = 64;
   } else {
     int nb_out = 0;
@@ -282,7 +287,7 @@ static Cost b200_dwpw(const Layer& d, const Layer& p, ll N, int dt, ll b, const 
   const ll Co = p.Cout;
   Geo g = geo_of(d, N, Co);
   ll bn;
-  if (dt == FCM_F32) {
+  if (dt == FCM_F32 || !aligned16(d.C, b) || !aligned16(Co, b)) {
     g.nb = 1; g.th = 8; g.tw = 8; bn = 64;
   } else {
     default_dwpw_tile(g);
@@ -308,7 +313,7 @@ static Cost b200_pwdw(const Layer& p, const Layer& d, ll N, int dt, ll b, const 
   Geo g = geo_of(d, N, Cm);
   g.C = (int)Cin;
   ll td;
-  if (dt == FCM_F32) {
+  if (dt == FCM_F32 || !aligned16(Cin, b) || !aligned16(Cm, b)) {
     g.nb = 1; g.th = 8; g.tw = 8; td = 32;
   } else {
     default_pwdw_tile(g);

@@ -11,6 +11,7 @@
 // Accumulators live in TMEM, double-buffered so the epilogue of tile i overlaps tile i+1.
 // One 32-bit word of channels per lane; a K chunk is one 128-byte row (64 bf16 / 128 int8).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -23,41 +24,69 @@ template <int DT> struct TcKind;
 template <> struct TcKind<FCM_BF16> { static constexpr MmaKind kind = MmaKind::F16; static constexpr uint32_t cf = 1, ab = 1; };
 template <> struct TcKind<FCM_F16> { static constexpr MmaKind kind = MmaKind::F16; static constexpr uint32_t cf = 1, ab = 0; };
 template <> struct TcKind<FCM_S8> { static constexpr MmaKind kind = MmaKind::I8; static constexpr uint32_t cf = 2, ab = 1; };
+// K elements per tcgen05.mma instruction (32 bytes of each operand row)
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
+// Pack two fp32 into bf16x2 / f16x2 (RNE), optionally with the free ReLU of cvt.relu.
+template <int DT, bool kRelu>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  uint32_t d;
+  if constexpr (DT == FCM_BF16) {
+    if constexpr (kRelu) asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    else asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  } else {
+    if constexpr (kRelu) asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    else asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  }
+  return d;
+}
+
 // Epilogue of 16 accumulator columns [n_base, n_base+16) of one row -> packed storage words.
+// Constants come from smem as 128-bit broadcast loads (n_base is a multiple of 16).
 template <int DT>
-__device__ __forceinline__ void epi16(const uint32_t (&r)[16], const EpiS& cs, const Epi& e, int n_base,
+__device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
                                       uint32_t (&out)[8]) {
   if constexpr (DT == FCM_S8) {
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
+      const uint4 bq = lds128(cs.base + 4 * (n_base + 4 * w));
+      const uint4 mq = lds128(cs.base + 4 * (cs.ncap + n_base + 4 * w));
+      const uint4 sh = lds128(cs.base + 4 * (2 * cs.ncap + n_base + 4 * w));
+      const uint32_t b4[4] = {bq.x, bq.y, bq.z, bq.w}, m4[4] = {mq.x, mq.y, mq.z, mq.w}, s4[4] = {sh.x, sh.y, sh.z, sh.w};
       uint32_t word = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int n = n_base + 4 * w + i;
-        EpiC c{0.f, 0.f, cs.bq(n), cs.mq(n), cs.sh(n)};
+        EpiC c{0.f, 0.f, (int32_t)b4[i], (int32_t)m4[i], (int32_t)s4[i]};
         const int32_t q = requant_i8(static_cast<int32_t>(r[4 * w + i]), c, e.zp_out, e.qmin, e.qmax);
         word |= (static_cast<uint32_t>(q) & 0xFFu) << (8 * i);
       }
       out[w] = word;
     }
   } else {
+    float sc[16], bi[16];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const int n = n_base + 2 * w;
-      const float v0 = epi_f(__uint_as_float(r[2 * w]), cs.sc(n), cs.bi(n), e.act);
-      const float v1 = epi_f(__uint_as_float(r[2 * w + 1]), cs.sc(n + 1), cs.bi(n + 1), e.act);
-      if constexpr (DT == FCM_BF16) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
-        out[w] = *reinterpret_cast<uint32_t*>(&h);
-      } else {
-        __half2 h = __floats2half2_rn(v0, v1);
-        out[w] = *reinterpret_cast<uint32_t*>(&h);
-      }
+    for (int q = 0; q < 4; ++q) {
+      const uint4 a = lds128(cs.base + 4 * (n_base + 4 * q));
+      const uint4 b = lds128(cs.base + 4 * (cs.ncap + n_base + 4 * q));
+      sc[4 * q] = __uint_as_float(a.x); sc[4 * q + 1] = __uint_as_float(a.y);
+      sc[4 * q + 2] = __uint_as_float(a.z); sc[4 * q + 3] = __uint_as_float(a.w);
+      bi[4 * q] = __uint_as_float(b.x); bi[4 * q + 1] = __uint_as_float(b.y);
+      bi[4 * q + 2] = __uint_as_float(b.z); bi[4 * q + 3] = __uint_as_float(b.w);
+    }
+    const float hi_c = act_hi(e.act);
+    if (e.act == FCM_ACT_NONE) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        out[w] = pack2<DT, false>(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]),
+                                  fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]));
+    } else {
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        out[w] = pack2<DT, true>(fminf(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]), hi_c),
+                                 fminf(fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]), hi_c));
     }
   }
 }
@@ -120,6 +149,7 @@ __global__ void __launch_bounds__(320, 1)
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
+  constexpr int KSTEP = 32 / Tr<DT>::ES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* stage = smem;                         // 2 x 16 KB output staging
@@ -181,8 +211,8 @@ __global__ void __launch_bounds__(320, 1)
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(abuf + s * 16384));
           const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + s * BN * 128));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+          const int ksteps = min(4, (K - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
+          for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
           mma_commit(empty + s);
         }
         mma_commit(tfull + acc);
@@ -229,6 +259,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
+  constexpr int KSTEP = 32 / Tr<DT>::ES;
   constexpr int kDwpwNDW = dwpw_ndw<DT, K>();
   constexpr int WARP_TX = 4 + kDwpwNDW, WARP_TB = 5 + kDwpwNDW, WARP_MMA = 6 + kDwpwNDW;
   const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
@@ -326,8 +357,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(abuf + a * 16384));
           const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + sb * BN * 128));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+          const int ksteps = min(4, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
+          for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
           mma_commit(aempty + a);
           mma_commit(emptyB + sb);
         }
@@ -432,13 +463,16 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
 // the PW of tile i+1, its epilogue and the DW of tile i proceed concurrently.
 // =====================================================================================
 constexpr int kPwdwNDW = 8;
+// T-producer warps (TMEM -> T): 8 (two per TMEM lane quadrant) for 3x3, 4 for 5x5 (registers).
+template <int K> constexpr int pwdw_ntp() { return K == 3 ? 8 : 4; }
 
 template <int DT, int K, int S>
-__global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
+__global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     pwdw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                    const typename Tr<DT>::T* __restrict__ wdw, Epi ep, Epi ed, uint8_t* __restrict__ y, int N, int H,
                    int W, int Cin, int Ho, int Wo, int Cmid, int pt, int pl, int nb, int th, int tw, int tiles_x,
-                   int tiles_y, int stages, uint32_t tmem_cols, int ncap) {
+                   int tiles_y, int stages, int depth, uint32_t tmem_cols, int ncap, int dbg,
+                   unsigned long long* trace) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int V = Tr<DT>::VEC;
   constexpr int KC = 128 / ES;
@@ -446,7 +480,9 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
   constexpr int PITCH = 128 + 16;        // bytes per T row in smem (padded: conflict-free)
   constexpr int PW = PITCH / 4;
   constexpr MmaKind KIND = TcKind<DT>::kind;
-  constexpr int WARP_TMA = 4 + kPwdwNDW, WARP_MMA = 5 + kPwdwNDW;
+  constexpr int KSTEP = 32 / Tr<DT>::ES;
+  constexpr int NTP = pwdw_ntp<K>();
+  constexpr int WARP_TMA = NTP + kPwdwNDW, WARP_MMA = NTP + 1 + kPwdwNDW;
   const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
   const int R = nb * th_in * tw_in;
   const int MB = (R + 127) / 128;
@@ -457,17 +493,17 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
   const int nslice = (Cmid + TD - 1) / TD;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* tsm = smem + stages * stage_bytes;  // 2 T buffers
-  uint8_t* cst = tsm + 2 * tbytes;
+  uint8_t* tsm = smem + stages * stage_bytes;  // `depth` T buffers
+  uint8_t* cst = tsm + depth * tbytes;
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(ncap));
   uint64_t* full = reinterpret_cast<uint64_t*>(wsm + K * K * nslice * 32);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* Tfull = tempty + 2;
-  uint64_t* Tempty = Tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(Tempty + 2);
+  uint64_t* tempty = tfull + 4;
+  uint64_t* Tfull = tempty + 4;
+  uint64_t* Tempty = Tfull + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(Tempty + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cmid, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cmid, ncap, dcst);
@@ -476,10 +512,10 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < depth; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, 128);
-      mbar_init(Tfull + a, 128);
+      mbar_init(tempty + a, NTP * 32);
+      mbar_init(Tfull + a, NTP * 32);
       mbar_init(Tempty + a, kPwdwNDW * 32);
     }
     fence_barrier_init();
@@ -494,6 +530,10 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
   const int total = spatial * nslice;
   const uint32_t acc_cols = MB * TD;
 
+  // development tracing (FCM_TRACE): clock64 stamps of CTA 0's first 64 tiles
+  auto stamp = [&](int local, int ev) {
+    if (trace && blockIdx.x == 0 && local < 64) trace[local * 16 + ev] = clock64();
+  };
   auto decode = [&](int t, int& sl, int& nbi, int& tyi, int& txi) {
     sl = t % nslice;
     int sp = t / nslice;
@@ -513,7 +553,12 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % stages;
           mbar_wait(empty + s, ((it / stages) & 1) ^ 1);
+          if (kc == 0) stamp(it / nk, 8);
           uint8_t* st = smem + s * stage_bytes;
+          if (dbg & 8) {
+            mbar_arrive(full + s);
+            continue;
+          }
           mbar_arrive_expect_tx(full + s, tx);
           tma_load_4d(st, &tmx, full + s, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
           tma_load_2d(st + astride, &tmb, full + s, kc * KC, sl * TD);
@@ -525,45 +570,51 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
       const uint32_t idesc = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, TD);
       int it = 0, local = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-        const int acc = local & 1;
-        mbar_wait(tempty + acc, ((local >> 1) & 1) ^ 1);
+        const int acc = local % depth;
+        mbar_wait(tempty + acc, ((local / depth) & 1) ^ 1);
+        stamp(local, 0);
         tc_fence_after();
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % stages;
           mbar_wait(full + s, (it / stages) & 1);
+          if (kc == 0) stamp(local, 1);
           tc_fence_after();
           uint8_t* st = smem + s * stage_bytes;
           const uint64_t bd = smem_desc_sw128(smem_u32(st + astride));
           for (int mb = 0; mb < MB; ++mb) {
             const uint64_t ad = smem_desc_sw128(smem_u32(st + mb * 16384));
             const uint32_t d = tbase + acc * acc_cols + mb * TD;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+            const int ksteps = min(4, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
+            for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
           }
           mma_commit(empty + s);
         }
         mma_commit(tfull + acc);
+        stamp(local, 2);
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < NTP) {
     // ---------------- T producers: TMEM (PW accumulators over the halo) -> eps_pw -> T (0 outside)
-    const int q = warp;
+    constexpr int G = NTP / 4;  // warps per TMEM lane quadrant, splitting the 16-column chunks
+    const int q = warp & 3, h = warp >> 2;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const int acc = local & 1;
+      const int acc = local % depth;
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       uint8_t* tb = tsm + acc * tbytes;
-      mbar_wait(tfull + acc, (local >> 1) & 1);
-      mbar_wait(Tempty + acc, ((local >> 1) & 1) ^ 1);
+      mbar_wait(tfull + acc, (local / depth) & 1);
+      if (warp == 0 && lane == 0) stamp(local, 3);
+      mbar_wait(Tempty + acc, ((local / depth) & 1) ^ 1);
+      if (warp == 0 && lane == 0) stamp(local, 4);
       tc_fence_after();
-      for (int mb = 0; mb < MB; ++mb) {
+      for (int mb = 0; mb < MB && !(dbg & 2); ++mb) {
         const int r = mb * 128 + q * 32 + lane;
         const int b = r / (th_in * tw_in), rr = r - b * th_in * tw_in;
         const int yi = tyi * th * S - pt + rr / tw_in, xi = txi * tw * S - pl + rr % tw_in;
         const int n = nbi * nb + b;
         const bool inside = (r < R) && (n < N) && (yi >= 0) && (yi < H) && (xi >= 0) && (xi < W);
-        for (int c0 = 0; c0 < TD; c0 += 16) {
+        for (int c0 = 16 * h; c0 < TD; c0 += 16 * G) {
           uint32_t rg[16];
           tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + acc * acc_cols + mb * TD + c0, rg);
           tmem_ld_wait();
@@ -579,19 +630,20 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
       tc_fence_before();
       mbar_arrive(tempty + acc);
       mbar_arrive(Tfull + acc);
+      if (warp == 0 && lane == 0) stamp(local, 5);
     }
   } else {
     // ---------------- DW consumers: T tile -> DW -> eps_dw -> OFM (128 B per warp store)
     constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
     constexpr int kSeg = kPair ? (S == 1 ? 8 : 4) : 8;
-    const int dw = warp - 4;
+    const int dw = warp - NTP;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
     const float lo_c = act_lo(ed.act), hi_c = act_hi(ed.act);
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const int tbi = local & 1;
+      const int tbi = local % depth;
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       const int c = sl * TD + lane * V;
@@ -603,8 +655,9 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
         load_dw_weights2_smem<DT, K>(W2, wsm, nslice * 32, sl * 32 + lane);
         const uint64_t sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1)), bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
         const bool cval = c < Cmid;
-        mbar_wait(Tfull + tbi, (local >> 1) & 1);
-        for (int item = dw; item < nitems; item += kPwdwNDW) {
+        mbar_wait(Tfull + tbi, (local / depth) & 1);
+        if (dw == 0 && lane == 0) stamp(local, 6);
+        for (int item = dw; item < nitems && !(dbg & 1); item += kPwdwNDW) {
           const int col = item / nseg, seg = item - col * nseg;
           const int b = col / tw, x = col - b * tw;
           const int n = nbi * nb + b, xo = txi * tw + x;
@@ -624,7 +677,7 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
         EpiC ec[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
-        mbar_wait(Tfull + tbi, (local >> 1) & 1);
+        mbar_wait(Tfull + tbi, (local / depth) & 1);
         for (int item = dw; item < nitems; item += kPwdwNDW) {
           const int col = item / nseg, seg = item - col * nseg;
           const int b = col / tw, x = col - b * tw;
@@ -642,6 +695,7 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
         }
       }
       mbar_arrive(Tempty + tbi);
+      if (dw == 0 && lane == 0) stamp(local, 7);
     }
   }
   __syncthreads();
@@ -657,6 +711,33 @@ __global__ void __launch_bounds__((4 + kPwdwNDW + 2) * 32, 1)
 static int debug_flags() {
   static int f = [] { const char* e = getenv("FCM_DEBUG_FLAGS"); return e ? atoi(e) : 0; }();
   return f;
+}
+
+// FCM_TRACE=<file> (development only): clock64 stamps of CTA 0 appended to <file> after each launch.
+static unsigned long long* trace_buf() {
+  static unsigned long long* buf = nullptr;
+  static bool on = getenv("FCM_TRACE") != nullptr;
+  if (on && !buf) {
+    cudaMalloc(&buf, 64 * 16 * sizeof(unsigned long long));
+    cudaMemset(buf, 0, 64 * 16 * sizeof(unsigned long long));
+  }
+  return on ? buf : nullptr;
+}
+static void trace_dump(const char* tag) {
+  unsigned long long* b = trace_buf();
+  if (!b) return;
+  unsigned long long h[64 * 16];
+  cudaDeviceSynchronize();
+  cudaMemcpy(h, b, sizeof(h), cudaMemcpyDeviceToHost);
+  FILE* f = fopen(getenv("FCM_TRACE"), "a");
+  if (!f) return;
+  fprintf(f, "# %s\n", tag);
+  for (int t = 0; t < 64; ++t) {
+    for (int e = 0; e < 10; ++e) fprintf(f, "%llu ", h[t * 16 + e]);
+    fprintf(f, "\n");
+  }
+  fclose(f);
+  cudaMemset(b, 0, sizeof(h));
 }
 
 static uint32_t pow2_cols(uint32_t c) {
@@ -829,22 +910,28 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   const int tbytes = ((R * (128 + 16)) + 1023) & ~1023;
   const int ncap = round_up(g.Cout, TD);
   const int nslice = ncap / TD;
-  const int fixed = 1024 + 2 * tbytes + 2 * consts_bytes<DT>(ncap) + K * K * nslice * 128 + 256;
-  const int budget = device_props().smem_optin - fixed;
-  const int stages = std::min(4, budget / stage_bytes);
+  const int depth = std::min(3, 512 / (MB * TD));  // TMEM accumulators = T buffers in flight
+  const int fixed = 1024 + 2 * consts_bytes<DT>(ncap) + K * K * nslice * 128 + 512;
+  int stages = 0, dep = depth;
+  for (; dep >= 2; --dep) {
+    stages = std::min(4, (device_props().smem_optin - fixed - dep * tbytes) / stage_bytes);
+    if (stages >= 2) break;
+  }
   if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pwdw_r: tile too large for 2 smem stages");
-  const size_t smem = (size_t)fixed + (size_t)stages * stage_bytes;
+  const size_t smem = (size_t)fixed + (size_t)dep * tbytes + (size_t)stages * stage_bytes;
   auto kern = pwdw_tc_kernel<DT, K, S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nslice;
   const int grid = std::min(total, device_props().sms);
   using TT = typename Tr<DT>::T;
-  kern<<<grid, (4 + kPwdwNDW + 2) * 32, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ep, ed,
+  kern<<<grid, (pwdw_ntp<K>() + kPwdwNDW + 2) * 32, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ep, ed,
                                                      static_cast<uint8_t*>(y), g.N, g.H, g.W, g.C, g.Ho, g.Wo, g.Cout,
-                                                     g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages,
-                                                     pow2_cols(2 * MB * TD), ncap);
-  return check_launch("pwdw_tc_kernel");
+                                                     g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages, dep,
+                                                     pow2_cols(dep * MB * TD), ncap, debug_flags(), trace_buf());
+  const int rc = check_launch("pwdw_tc_kernel");
+  trace_dump("pwdw");
+  return rc;
 }
 
 template <int DT>

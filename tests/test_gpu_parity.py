@@ -51,8 +51,6 @@ def test_dw_nchw():
 @pytest.mark.parametrize("fmt", ["f32", "bf16", "f16", "s8"])
 @pytest.mark.parametrize("c_in,c_out", [(16, 32), (40, 24), (144, 24), (320, 1280), (96, 576)])
 def test_pw(fmt, c_in, c_out):
-    if fmt == "s8" and (c_in % 16 or c_out % 16):
-        pytest.skip("int8 needs 16-byte channel pitch")
     Case("pw", fmt, 2, 13, 11, c_in, c_out).check()
 
 
@@ -117,10 +115,20 @@ def test_int8_fused_equals_unfused_bitwise():
 def test_abi_errors_on_gpu():
     import paper_2404_19331_b200 as fcm
     from paper_2404_19331_b200._lib import FcmError
-    x = torch.zeros(1, 8, 8, 24, dtype=torch.int8, device="cuda")  # 24-byte pitch: not 16-B aligned
-    w = torch.zeros(3, 3, 24, dtype=torch.int8, device="cuda")
-    ep = fcm.Epilogue(mult_q=torch.ones(24, dtype=torch.int32, device="cuda"),
-                      shift_q=torch.ones(24, dtype=torch.int32, device="cuda"))
+    x = torch.zeros(1, 8, 8, 32, dtype=torch.int8, device="cuda")
+    w = torch.zeros(3, 3, 32, dtype=torch.int8, device="cuda")
+    ep = fcm.Epilogue(mult_q=torch.ones(32, dtype=torch.int32, device="cuda"),
+                      shift_q=torch.ones(32, dtype=torch.int32, device="cuda"), zp_in=3)
     with pytest.raises(FcmError) as e:
         fcm.dw(x, w, 1, None, ep)
-    assert e.value.status == -2
+    assert e.value.status == -3  # nonzero input zero point: FCM_E_UNSUPPORTED on the GPU path
+
+
+# ---------------------------------------------------------------- unaligned channel pitch (CUDA-core paths)
+# EfficientNet-B0 int8 has C = 24 / 40: a 24- or 40-byte NHWC pitch, which TMA cannot address.
+@pytest.mark.parametrize("fmt", ["s8", "bf16"])
+def test_unaligned_pitch_layers(fmt):
+    Case("dw", fmt, 2, 13, 11, 40 if fmt == "s8" else 12, k=5, s=2).check()
+    Case("pw", fmt, 2, 9, 7, 144, 40 if fmt == "s8" else 12).check()
+    Case("dwpw", fmt, 2, 14, 14, 240 if fmt == "s8" else 36, 40 if fmt == "s8" else 12, k=5, s=1).check()
+    Case("pwdw", fmt, 2, 15, 13, 24 if fmt == "s8" else 12, 144 if fmt == "s8" else 36, k=5, s=2).check()
