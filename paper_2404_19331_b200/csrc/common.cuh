@@ -161,29 +161,38 @@ struct EpiS {
   __device__ __forceinline__ int32_t sh(int n) const { return (int32_t)lds32(base + 4 * (2 * ncap + n)); }
 };
 
-// Fill the constant arrays for columns [0, ncap) (zeros past N).
+// Fill the constant arrays for columns [0, ncap) (zeros past N). Each thread first issues up to
+// 4 independent global loads per array, then the shared stores (no load/store serialisation).
 template <int DT>
 __device__ __forceinline__ EpiS stage_consts(const Epi& e, int N, int ncap, uint8_t* area) {
-  if constexpr (DT == FCM_S8) {
-    int32_t* bq = reinterpret_cast<int32_t*>(area);
-    int32_t* mq = bq + ncap;
-    int32_t* sh = mq + ncap;
-    for (int i = threadIdx.x; i < ncap; i += blockDim.x) {
+  const uint32_t base = smem_u32(area);
+  const int nt = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < ncap; i0 += 4 * nt) {
+    uint32_t a[4], b[4], c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * nt;
       const bool v = i < N;
-      bq[i] = (v && e.bias_q) ? e.bias_q[i] : 0;
-      mq[i] = v ? e.mult_q[i] : 0;
-      sh[i] = v ? e.shift_q[i] : 1;
+      if constexpr (DT == FCM_S8) {
+        a[u] = (v && e.bias_q) ? (uint32_t)__ldg(e.bias_q + i) : 0u;
+        b[u] = v ? (uint32_t)__ldg(e.mult_q + i) : 0u;
+        c[u] = v ? (uint32_t)__ldg(e.shift_q + i) : 1u;
+      } else {
+        a[u] = __float_as_uint(v ? (e.scale ? __ldg(e.scale + i) : 1.f) : 0.f);
+        b[u] = __float_as_uint((v && e.bias) ? __ldg(e.bias + i) : 0.f);
+      }
     }
-  } else {
-    float* sc = reinterpret_cast<float*>(area);
-    float* bi = sc + ncap;
-    for (int i = threadIdx.x; i < ncap; i += blockDim.x) {
-      const bool v = i < N;
-      sc[i] = v ? (e.scale ? e.scale[i] : 1.f) : 0.f;
-      bi[i] = (v && e.bias) ? e.bias[i] : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * nt;
+      if (i < ncap) {
+        sts32(base + 4 * i, a[u]);
+        sts32(base + 4 * (ncap + i), b[u]);
+        if constexpr (DT == FCM_S8) sts32(base + 4 * (2 * ncap + i), c[u]);
+      }
     }
   }
-  return EpiS{smem_u32(area), ncap};
+  return EpiS{base, ncap};
 }
 template <int DT> constexpr int consts_bytes(int ncap) { return (DT == FCM_S8 ? 12 : 8) * ncap; }
 
@@ -363,9 +372,19 @@ template <int DT>
 __device__ __forceinline__ void stage_dw_weights(const void* wdw, int k, int C, int cwords, uint32_t* wsm) {
   const uint32_t* g = static_cast<const uint32_t*>(wdw);
   const int cw_real = C / Tr<DT>::VEC;
-  for (int i = threadIdx.x; i < k * k * cwords; i += blockDim.x) {
-    const int t = i / cwords, w = i - t * cwords;
-    wsm[i] = (w < cw_real) ? g[t * cw_real + w] : 0u;
+  const int n = k * k * cwords, nt = blockDim.x;
+  const uint32_t base = smem_u32(wsm);
+  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * nt) {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * nt;
+      const int t = i / cwords, w = i - t * cwords;
+      v[u] = (i < n && w < cw_real) ? __ldg(g + t * cw_real + w) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * nt < n) sts32(base + 4 * (i0 + u * nt), v[u]);
   }
 }
 

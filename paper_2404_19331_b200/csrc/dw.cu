@@ -45,27 +45,34 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
   uint32_t* yw = reinterpret_cast<uint32_t*>(y);
   constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
   if constexpr (kPair) {
-    // same paired-FP32 core and segment length as the fused kernels (bit-identical DW)
+    // same paired-FP32 core and segment length as the fused kernels (bit-identical DW); a partly
+    // filled channel group packs 2 or 4 output columns per warp (gs lanes per pixel)
     constexpr int kSeg = (S == 1) ? 4 : 2;
+    const int cw_valid = min(32, (C - c0) / V);
+    const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+    const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+    const int cl = c0 + wd * V;
+    const bool cval = wd < cw_valid;
     DwW2<DT, K> W2;
-    load_dw_weights2<DT, K>(W2, wdw, C, c);
-    const bool cval = c < C;
-    const uint64_t sc2 = f2_pack(cval ? (ep.scale ? ep.scale[c] : 1.f) : 0.f, cval ? (ep.scale ? ep.scale[c + 1] : 1.f) : 0.f);
-    const uint64_t bi2 = f2_pack(cval && ep.bias ? ep.bias[c] : 0.f, cval && ep.bias ? ep.bias[c + 1] : 0.f);
+    load_dw_weights2<DT, K>(W2, wdw, C, cval ? cl : C);
+    const uint64_t sc2 = f2_pack(cval ? (ep.scale ? ep.scale[cl] : 1.f) : 0.f, cval ? (ep.scale ? ep.scale[cl + 1] : 1.f) : 0.f);
+    const uint64_t bi2 = f2_pack(cval && ep.bias ? ep.bias[cl] : 0.f, cval && ep.bias ? ep.bias[cl + 1] : 0.f);
     const float lo_c = act_lo(ep.act), hi_c = act_hi(ep.act);
     mbar_wait(&bar, 0);
     const int nseg = (nrows + kSeg - 1) / kSeg;
-    for (int item = warp; item < tw * nseg; item += 4) {
-      const int col = item / nseg, seg = item - col * nseg;
+    const int ncolg = (tw + npix - 1) / npix;
+    for (int item = warp; item < ncolg * nseg; item += 4) {
+      const int cg = item / nseg, seg = item - cg * nseg;
+      const int col = cg * npix + grp;
       const int x = x0 + col;
-      if (x >= Wo) continue;
+      const bool live = col < tw && x < Wo && cval;
       const int ys = seg * kSeg;
-      const uint32_t src = smem_u32(xs) + ((col * S) * 32 + lane) * 4;
-      uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + x) * C + c) / V;
+      const uint32_t src = smem_u32(xs) + (((live ? col : 0) * S) * 32 + wd) * 4;
+      uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + (live ? x : 0)) * C + cl) / V;
       const size_t rstride = (size_t)Wo * C / V;
-      const int nvalid = nrows - ys;
+      const int nvalid = live ? nrows - ys : 0;
       dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
-        if (r < nvalid && cval) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
+        if (r < nvalid) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
       });
     }
     return;

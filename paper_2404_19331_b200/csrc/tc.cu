@@ -145,7 +145,7 @@ template <int DT>
 __global__ void __launch_bounds__(320, 1)
     pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                  const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, int stages,
-                 uint32_t tmem_cols, int ncap) {
+                 uint32_t tmem_cols, int ncap, unsigned long long* trace) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
@@ -180,16 +180,20 @@ __global__ void __launch_bounds__(320, 1)
   const int nbm = (M + 127) / 128;
   const int total = nbm * nbn;
   const uint32_t stage_tx = 16384 + BN * 128;
+  auto stamp = [&](int local, int ev) {
+    if (trace && blockIdx.x == 0 && local < 64) trace[local * 16 + ev] = clock64();
+  };
 
   if (warp == 8) {
     if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
         const int m0 = (t / nbn) * 128, n0 = (t % nbn) * BN;
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(empty + s, ph ^ 1);
+          if (kc == 0) stamp(lt, 8);
           mbar_arrive_expect_tx(full + s, stage_tx);
           tma_load_2d(abuf + s * 16384, &tma, full + s, kc * KC, m0);
           tma_load_2d(bbuf + s * BN * 128, &tmb, full + s, kc * KC, n0);
@@ -203,11 +207,13 @@ __global__ void __launch_bounds__(320, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local & 1;
         mbar_wait(tempty + acc, ((local >> 1) & 1) ^ 1);
+        stamp(local, 0);
         tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % stages;
           mbar_wait(full + s, (it / stages) & 1);
+          if (kc == 0) stamp(local, 1);
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(abuf + s * 16384));
           const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + s * BN * 128));
@@ -216,6 +222,7 @@ __global__ void __launch_bounds__(320, 1)
           mma_commit(empty + s);
         }
         mma_commit(tfull + acc);
+        stamp(local, 2);
       }
     }
   } else {
@@ -224,11 +231,13 @@ __global__ void __launch_bounds__(320, 1)
       const int acc = local & 1;
       const int m0 = (t / nbn) * 128, n0 = (t % nbn) * BN;
       mbar_wait(tfull + acc, (local >> 1) & 1);
+      if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
       epilogue_tile<DT, 8>(tbase + acc * BN, BN, n0, N, cs, ep, stage, sbuf,
                            [&](const uint8_t* buf, int c) { tma_store_2d(&tmy, buf, c, m0); });
       tc_fence_before();
       mbar_arrive(tempty + acc);
+      if (threadIdx.x == 0) stamp(local, 5);
     }
     if (threadIdx.x == 0) bulk_wait_all();
   }
@@ -288,6 +297,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   const EpiS cs = stage_consts<DT>(ep, Cout, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cin, nk * KC, dcst);
   stage_dw_weights<DT>(wdw, K, Cin, nk * 32, wsm);
+  for (int i = threadIdx.x; i < kDwpwNA * 16384 / 16; i += blockDim.x) sts128(smem_u32(abuf) + 16 * i, 0, 0, 0, 0);
   if (warp == WARP_TX && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
@@ -381,26 +391,54 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
         const uint32_t st = smem_u32(xbuf + sx * xstride);
         const uint32_t abase = smem_u32(abuf + a * 16384);
         if constexpr (kPair) {
+          // lane groups: a partially filled chunk (C_in not a multiple of 64) packs 2 or 4 output
+          // columns into one warp (gs lanes per pixel) instead of idling the empty lanes
+          const int cw_valid = min(32, (Cin - kc * KC) / V);
+          const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+          const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+          const int cl = kc * KC + wd * V;
           DwW2<DT, K> W2;
-          load_dw_weights2_smem<DT, K>(W2, wsm, nk * 32, kc * 32 + lane);
-          const uint64_t sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1)), bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
-          const bool cval = c < Cin;
+          load_dw_weights2_smem<DT, K>(W2, wsm, nk * 32, kc * 32 + wd);
+          const uint64_t sc2 = f2_pack(dcs.sc(cl), dcs.sc(cl + 1)), bi2 = f2_pack(dcs.bi(cl), dcs.bi(cl + 1));
+          const bool cval = wd < cw_valid;
           const float lo_c = act_lo(ed.act), hi_c = act_hi(ed.act);
+          const int ncolg = (nb * tw + npix - 1) / npix;
+          const int nitems_g = ncolg * nseg;
           mbar_wait(fullX + sx, (it / XS) & 1);
           mbar_wait(aempty + a, ((it / kDwpwNA) & 1) ^ 1);
-          for (int item = dw; item < nitems && !(dbg & 1); item += kDwpwNDW) {
-            const int col = item / nseg, seg = item - col * nseg;
-            const int b = col / tw, x = col - b * tw;
-            const int y0 = seg * kSeg;
-            const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
-            const int mbase = (b * th + y0) * tw + x;
-            const int nvalid = th - y0;
-            dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
-              if (r < nvalid) {
-                const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
-                sts32(abase + sw128_off(mbase + r * tw, lane), word);
-              }
-            });
+          if (gs == 32) {  // full chunk: one output column per warp
+            for (int item = dw; item < nitems && !(dbg & 1); item += kDwpwNDW) {
+              const int col = item / nseg, seg = item - col * nseg;
+              const int b = col / tw, x = col - b * tw;
+              const int y0 = seg * kSeg;
+              const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
+              const int mbase = (b * th + y0) * tw + x;
+              const int nvalid = th - y0;
+              dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+                if (r < nvalid) {
+                  const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
+                  sts32(abase + sw128_off(mbase + r * tw, lane), word);
+                }
+              });
+            }
+          } else {
+            for (int item = dw; item < nitems_g && !(dbg & 1); item += kDwpwNDW) {
+              const int cg = item / nseg, seg = item - cg * nseg;
+              const int colr = cg * npix + grp;
+              const bool live = colr < nb * tw;
+              const int col = live ? colr : 0;
+              const int b = col / tw, x = col - b * tw;
+              const int y0 = seg * kSeg;
+              const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + wd) * 4;
+              const int mbase = (b * th + y0) * tw + x;
+              const int nvalid = live ? th - y0 : 0;
+              dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+                if (r < nvalid) {
+                  const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
+                  sts32(abase + sw128_off(mbase + r * tw, wd), word);
+                }
+              });
+            }
           }
         } else {
           DwW<DT, K> W;
@@ -794,8 +832,10 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int total = ((M + 127) / 128) * nbn;
   const int grid = std::min(total, device_props().sms);
-  kern<<<grid, 320, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, stages, pow2_cols(2 * BN), ncap);
-  return check_launch("pw_tc_kernel");
+  kern<<<grid, 320, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, stages, pow2_cols(2 * BN), ncap, trace_buf());
+  const int rc = check_launch("pw_tc_kernel");
+  trace_dump("pw");
+  return rc;
 }
 
 int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st) {
