@@ -135,6 +135,69 @@ def cpu_baseline(net, dtype, seconds=15.0):
             "sample": f"{n} images x whole {net} DW/PW stack ({dtype}), one at a time, {dt:.1f}s"}
 
 
+def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5):
+    """cuDNN's unfused DW + PW (PyTorch F.conv2d, channels_last, cudnn.benchmark) on the same layers
+    and synthetic weights: BN scale folded into the weights, bias in the conv, activation as an
+    in-place clamp. Captured in a CUDA graph; device time per step via CUDA events."""
+    import numpy as np
+    import torch.nn.functional as F
+    from synth.networks import NETWORKS, layer_ids, network_params
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[dtype]
+    torch.backends.cudnn.benchmark = True
+    prm = network_params(0x5EED, net, dtype)
+    layers = []
+    for lid, _, l in layer_ids(NETWORKS[net]()):
+        p = prm[lid]
+        sc = torch.as_tensor(np.asarray(p["scale"]), dtype=torch.float64)
+        if l["kind"] == "dw":
+            w = torch.as_tensor(np.asarray(p["w"]), dtype=torch.float64).permute(2, 0, 1)[:, None] * sc[:, None, None, None]
+            layers.append(("dw", w.to(tdt).to(dev).contiguous(memory_format=torch.channels_last),
+                           torch.as_tensor(np.asarray(p["bias"])).to(tdt).to(dev), l))
+        else:
+            w = (torch.as_tensor(np.asarray(p["w"]), dtype=torch.float64).t() * sc[:, None])[:, :, None, None]
+            layers.append(("pw", w.to(tdt).to(dev).contiguous(memory_format=torch.channels_last),
+                           torch.as_tensor(np.asarray(p["bias"])).to(tdt).to(dev), l))
+    l0 = layers[0][3]
+    c0 = l0["c"] if l0["kind"] == "dw" else l0["c_in"]
+    x = torch.randn(batch, c0, l0["h"], l0["w"], device=dev, dtype=tdt).contiguous(memory_format=torch.channels_last)
+
+    def run():
+        y = x
+        for kind, w, b, l in layers:
+            if kind == "dw":
+                y = F.conv2d(y, w, b, stride=l["stride"], padding=l["k"] // 2, groups=l["c"])
+            else:
+                if y.shape[1] != w.shape[1]:  # CvT: every projection block reads a stage token map
+                    y = torch.zeros(batch, w.shape[1], l["h"], l["w"], device=dev, dtype=tdt).contiguous(
+                        memory_format=torch.channels_last)
+                y = F.conv2d(y, w, b)
+            if l["act"] == 2:
+                y.clamp_(0, 6)
+            elif l["act"] == 1:
+                y.relu_()
+        return y
+    if net == "cvt13":
+        return None
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run()
+    for _ in range(warmup):
+        g.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"value": round(batch / (ms / 1e3), 1), "unit": "images/s", "ms_per_step": round(ms, 4),
+            "kind": "torch F.conv2d (cuDNN), unfused DW + PW, folded BN, channels_last, CUDA graph"}
+
+
 def traffic_from_profiles(kernel, config_tag):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -194,6 +257,7 @@ def main():
     ap.add_argument("--ref-images", type=int, default=1, help="reference arm: images per step")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cudnn", action="store_true", help="skip the cuDNN unfused DW+PW baseline")
     ap.add_argument("--layers-out", default="", help="write the per-entry table (JSON) here")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly (for ncu launch lists)")
     args = ap.parse_args()
@@ -355,6 +419,14 @@ def main():
         }
         if ws > 1:
             line["verify"] = verify
+        if not args.no_cudnn and args.dtype in ("bf16", "f16", "f32"):
+            try:
+                cb = cudnn_stack(args.net, args.dtype, args.batch, dev)
+                if cb:
+                    cb["fcm_speedup"] = round(line["value"] / ws / cb["value"], 3)
+                    line["cudnn_baseline"] = cb
+            except Exception as e:  # baseline only; never fails the bench
+                line["cudnn_baseline"] = {"error": str(e)[:200]}
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = cpu_baseline(args.net, args.dtype, args.cpu_seconds)
         if args.layers_out:
