@@ -202,7 +202,8 @@ def traffic_from_profiles(kernel, config_tag):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(p))
-        return d.get(config_tag, {}).get(kernel)
+        t = d.get(config_tag, {}).get(kernel)
+        return None if t is None else round(t["traffic_bytes_per_launch"])
     except Exception:
         return None
 
