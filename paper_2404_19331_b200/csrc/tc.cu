@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(320, 1)
 // 128-byte chunks, so the intermediate "contains all channels" in time, not space.
 // =====================================================================================
 // DW warps per DWPW CTA: 16 for the paired-FP32 bf16/f16 3x3 core (fits 93 registers), else 8.
-template <int DT, int K> constexpr int dwpw_ndw() { return ((DT == FCM_BF16 || DT == FCM_F16) && K == 3) ? 16 : 8; }
+template <int DT, int K> constexpr int dwpw_ndw() { return 8; }
 constexpr int kDwpwNA = 2;  // A-operand (commBuffer) ring depth
 
 template <int DT, int K, int S>
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
     // ---------------- DW warps: X halo chunk (smem) -> DW -> eps_dw -> A operand (commBuffer)
     // work item = (output column, segment of kSeg rows), round-robin over the DW warps
     constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
-    constexpr int kSeg = kPair ? (S == 1 ? 4 : 2) : 8;
+    constexpr int kSeg = kPair ? (S == 1 ? 8 : 4) : 8;
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
