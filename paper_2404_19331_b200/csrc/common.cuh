@@ -340,6 +340,68 @@ __device__ __forceinline__ void dw_seg2(uint32_t src, int col_bytes, int row_byt
   }
 }
 
+// Mixed-precision FMA on sm_100: fp32 accumulator += bf16/f16 x bf16/f16 taken straight from the
+// halves of packed 32-bit words (SASS FHFMA with .H0/.H1 selectors) -- no unpacking. Exact: the
+// product of two bf16/f16 values is exact in fp32, so the result equals fmaf on converted values.
+template <int DT>
+__device__ __forceinline__ void hfma2_acc(float& a0, float& a1, uint32_t x, uint32_t w) {
+  if constexpr (DT == FCM_BF16)
+    asm("{.reg .b16 xl, xh, wl, wh;\n\tmov.b32 {xl, xh}, %2;\n\tmov.b32 {wl, wh}, %3;\n\t"
+        "fma.rn.f32.bf16 %0, xl, wl, %0;\n\tfma.rn.f32.bf16 %1, xh, wh, %1;}"
+        : "+f"(a0), "+f"(a1) : "r"(x), "r"(w));
+  else
+    asm("{.reg .b16 xl, xh, wl, wh;\n\tmov.b32 {xl, xh}, %2;\n\tmov.b32 {wl, wh}, %3;\n\t"
+        "fma.rn.f32.f16 %0, xl, wl, %0;\n\tfma.rn.f32.f16 %1, xh, wh, %1;}"
+        : "+f"(a0), "+f"(a1) : "r"(x), "r"(w));
+}
+
+template <int K>
+struct DwWh {
+  uint32_t w[K][K];  // packed channel pairs
+};
+
+template <int K>
+__device__ __forceinline__ void load_dw_weights_h_smem(DwWh<K>& W, const uint32_t* wsm, int cwords, int cw) {
+  const uint32_t a = smem_u32(wsm) + 4 * cw;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) W.w[i][j] = lds32(a + 4 * (i * K + j) * cwords);
+}
+
+template <int K>
+__device__ __forceinline__ void load_dw_weights_h(DwWh<K>& W, const void* wdw, int C, int c) {
+  const uint32_t* g = static_cast<const uint32_t*>(wdw);
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) W.w[i][j] = (c < C) ? __ldg(g + (i * K + j) * (C / 2) + c / 2) : 0u;
+}
+
+// Same contract as dw_seg2 (rows y0..y0+SEG-1, input rows clamped to max_row), with the window and
+// the weights kept as packed words; sink(r, acc) receives the fp32 pair packed in a uint64.
+template <int DT, int K, int S, int SEG, class Sink>
+__device__ __forceinline__ void dw_segh(uint32_t src, int col_bytes, int row_bytes, int y0, int max_row,
+                                        const DwWh<K>& W, Sink&& sink) {
+  constexpr int WR = (SEG - 1) * S + K;
+  uint32_t win[WR][K];
+#pragma unroll
+  for (int i = 0; i < WR; ++i) {
+    const uint32_t rp = src + min(y0 * S + i, max_row) * row_bytes;
+#pragma unroll
+    for (int j = 0; j < K; ++j) win[i][j] = lds32(rp + j * col_bytes);
+  }
+#pragma unroll
+  for (int r = 0; r < SEG; ++r) {
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) hfma2_acc<DT>(a0, a1, win[r * S + i][j], W.w[i][j]);
+    sink(r, f2_pack(a0, a1));
+  }
+}
+
 // Epilogue of an fp32 pair -> packed bf16x2 / f16x2 word (scale/bias as pairs, clamp = activation).
 template <int DT>
 __device__ __forceinline__ uint32_t epi2_pack(uint64_t acc, uint64_t sc, uint64_t bi, float lo_c, float hi_c) {

@@ -53,8 +53,8 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
     const int cl = c0 + wd * V;
     const bool cval = wd < cw_valid;
-    DwW2<DT, K> W2;
-    load_dw_weights2<DT, K>(W2, wdw, C, cval ? cl : C);
+    DwWh<K> W2;
+    load_dw_weights_h<K>(W2, wdw, C, cval ? cl : C);
     const uint64_t sc2 = f2_pack(cval ? (ep.scale ? ep.scale[cl] : 1.f) : 0.f, cval ? (ep.scale ? ep.scale[cl + 1] : 1.f) : 0.f);
     const uint64_t bi2 = f2_pack(cval && ep.bias ? ep.bias[cl] : 0.f, cval && ep.bias ? ep.bias[cl + 1] : 0.f);
     const float lo_c = act_lo(ep.act), hi_c = act_hi(ep.act);
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
       uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + (live ? x : 0)) * C + cl) / V;
       const size_t rstride = (size_t)Wo * C / V;
       const int nvalid = live ? nrows - ys : 0;
-      dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
+      dw_segh<DT, K, S, kSeg>(src, 128, tw_in * 128, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
         if (r < nvalid) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
       });
     }

@@ -397,8 +397,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
           const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
           const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
           const int cl = kc * KC + wd * V;
-          DwW2<DT, K> W2;
-          load_dw_weights2_smem<DT, K>(W2, wsm, nk * 32, kc * 32 + wd);
+          DwWh<K> W2;
+          load_dw_weights_h_smem<K>(W2, wsm, nk * 32, kc * 32 + wd);
           const uint64_t sc2 = f2_pack(dcs.sc(cl), dcs.sc(cl + 1)), bi2 = f2_pack(dcs.bi(cl), dcs.bi(cl + 1));
           const bool cval = wd < cw_valid;
           const float lo_c = act_lo(ed.act), hi_c = act_hi(ed.act);
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
               const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
               const int mbase = (b * th + y0) * tw + x;
               const int nvalid = th - y0;
-              dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+              dw_segh<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
                 if (r < nvalid) {
                   const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
                   sts32(abase + sw128_off(mbase + r * tw, lane), word);
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
               const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + wd) * 4;
               const int mbase = (b * th + y0) * tw + x;
               const int nvalid = live ? th - y0 : 0;
-              dw_seg2<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+              dw_segh<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
                 if (r < nvalid) {
                   const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
                   sts32(abase + sw128_off(mbase + r * tw, wd), word);
@@ -689,8 +689,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       const int y0t = tyi * th;
       const int nrows_t = min(th, Ho - y0t);
       if constexpr (kPair) {
-        DwW2<DT, K> W2;
-        load_dw_weights2_smem<DT, K>(W2, wsm, nslice * 32, sl * 32 + lane);
+        DwWh<K> W2;
+        load_dw_weights_h_smem<K>(W2, wsm, nslice * 32, sl * 32 + lane);
         const uint64_t sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1)), bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
         const bool cval = c < Cmid;
         mbar_wait(Tfull + tbi, (local / depth) & 1);
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
           const int nvalid = nrows_t - y0;
           uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
           const size_t rstride = (size_t)Wo * Cmid / V;
-          dw_seg2<DT, K, S, kSeg>(src, PITCH, tw_in * PITCH, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+          dw_segh<DT, K, S, kSeg>(src, PITCH, tw_in * PITCH, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
             if (r < nvalid && cval) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
           });
         }
