@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
   if constexpr (kPair) {
     // same paired-FP32 core and segment length as the fused kernels (bit-identical DW); a partly
     // filled channel group packs 2 or 4 output columns per warp (gs lanes per pixel)
-    constexpr int kSeg = (S == 1) ? 8 : 4;
+    constexpr int kSeg = (S == 1) ? 16 : 8;
     const int cw_valid = min(32, (C - c0) / V);
     const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
     const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;

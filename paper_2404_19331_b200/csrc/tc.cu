@@ -12,6 +12,7 @@
 // One 32-bit word of channels per lane; a K chunk is one 128-byte row (64 bf16 / 128 int8).
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
     // ---------------- DW warps: X halo chunk (smem) -> DW -> eps_dw -> A operand (commBuffer)
     // work item = (output column, segment of kSeg rows), round-robin over the DW warps
     constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
-    constexpr int kSeg = kPair ? (S == 1 ? 8 : 4) : 8;
+    constexpr int kSeg = kPair ? (S == 1 ? 16 : 8) : 8;
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
@@ -406,40 +407,34 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
           const int nitems_g = ncolg * nseg;
           mbar_wait(fullX + sx, (it / XS) & 1);
           mbar_wait(aempty + a, ((it / kDwpwNA) & 1) ^ 1);
-          if (gs == 32) {  // full chunk: one output column per warp
-            for (int item = dw; item < nitems && !(dbg & 1); item += kDwpwNDW) {
-              const int col = item / nseg, seg = item - col * nseg;
-              const int b = col / tw, x = col - b * tw;
-              const int y0 = seg * kSeg;
-              const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
-              const int mbase = (b * th + y0) * tw + x;
-              const int nvalid = th - y0;
-              dw_segh<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
-                if (r < nvalid) {
-                  const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
-                  sts32(abase + sw128_off(mbase + r * tw, lane), word);
-                }
-              });
-            }
-          } else {
-            for (int item = dw; item < nitems_g && !(dbg & 1); item += kDwpwNDW) {
-              const int cg = item / nseg, seg = item - cg * nseg;
-              const int colr = cg * npix + grp;
+          // segment length adapted to the tile height (compile-time per variant)
+          auto run_items = [&](auto segc) {
+            constexpr int SEG = decltype(segc)::value;
+            const int nsg = (th + SEG - 1) / SEG;
+            const int ncg = (gs == 32) ? nb * tw : ncolg;
+            for (int item = dw; item < ncg * nsg && !(dbg & 1); item += kDwpwNDW) {
+              const int cg = item / nsg, seg = item - cg * nsg;
+              const int colr = (gs == 32) ? cg : cg * npix + grp;
               const bool live = colr < nb * tw;
               const int col = live ? colr : 0;
               const int b = col / tw, x = col - b * tw;
-              const int y0 = seg * kSeg;
+              const int y0 = seg * SEG;
               const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + wd) * 4;
               const int mbase = (b * th + y0) * tw + x;
               const int nvalid = live ? th - y0 : 0;
-              dw_segh<DT, K, S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
+              dw_segh<DT, K, S, SEG>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
                 if (r < nvalid) {
                   const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
                   sts32(abase + sw128_off(mbase + r * tw, wd), word);
                 }
               });
             }
-          }
+          };
+          // longest segment that still gives every DW warp an item (fewer window reloads)
+          const int ncg_ = (gs == 32) ? nb * tw : ncolg;
+          if (S == 1 && th > 8 && ncg_ * ((th + 15) / 16) >= kDwpwNDW) run_items(std::integral_constant<int, 16>());
+          else if (th > 4 && ncg_ * ((th + 7) / 8) >= kDwpwNDW / 2) run_items(std::integral_constant<int, 8>());
+          else run_items(std::integral_constant<int, 4>());
         } else {
           DwW<DT, K> W;
           load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + lane);
@@ -673,7 +668,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   } else {
     // ---------------- DW consumers: T tile -> DW -> eps_dw -> OFM (128 B per warp store)
     constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
-    constexpr int kSeg = kPair ? (S == 1 ? 8 : 4) : 8;
+    constexpr int kSeg = kPair ? (S == 1 ? 16 : 8) : 8;
     const int dw = warp - NTP;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
