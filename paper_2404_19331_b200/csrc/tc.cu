@@ -628,7 +628,9 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     }
   } else if (warp < NTP) {
     // ---------------- T producers: TMEM (PW accumulators over the halo) -> eps_pw -> T (0 outside)
-    constexpr int G = NTP / 4;  // warps per TMEM lane quadrant, splitting the 16-column chunks
+    constexpr int G = NTP / 4;      // warps per TMEM lane quadrant; each owns TD/G contiguous columns
+    constexpr int CPW = TD / G;     // 32 or 64 (bf16), 64 or 128 (int8)
+    constexpr int NU = CPW / 32;    // 32-column TMEM loads per M block
     const int q = warp & 3, h = warp >> 2;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -647,16 +649,21 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
         const int yi = tyi * th * S - pt + rr / tw_in, xi = txi * tw * S - pl + rr % tw_in;
         const int n = nbi * nb + b;
         const bool inside = (r < R) && (n < N) && (yi >= 0) && (yi < H) && (xi >= 0) && (xi < W);
-        for (int c0 = 16 * h; c0 < TD; c0 += 16 * G) {
-          uint32_t rg[16];
-          tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + acc * acc_cols + mb * TD + c0, rg);
-          tmem_ld_wait();
+#pragma unroll 1
+        for (int u = 0; u < NU; ++u) {
+          uint32_t rg[32];
+          tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * acc_cols + mb * TD + h * CPW + 32 * u, rg);
+          tmem_ld_wait();  // one round trip per 32 columns
           if (r < R) {
-            uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            if (inside) epi16<DT>(rg, cs, ep, sl * TD + c0, o);
-            const uint32_t dst = smem_u32(tb) + r * PITCH + c0 * ES;
 #pragma unroll
-            for (int v = 0; v < ES; ++v) sts128(dst + 16 * v, o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+            for (int hh = 0; hh < 2; ++hh) {
+              const int c0 = h * CPW + 32 * u + 16 * hh;
+              uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+              if (inside) epi16<DT>(&rg[16 * hh], cs, ep, sl * TD + c0, o);
+              const uint32_t dst = smem_u32(tb) + r * PITCH + c0 * ES;
+#pragma unroll
+              for (int v = 0; v < ES; ++v) sts128(dst + 16 * v, o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+            }
           }
         }
       }
