@@ -139,6 +139,49 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tacc, int BN, int n0, int
   }
 }
 
+// Warp-private epilogue (PW): warp w owns TMEM lane quadrant q = w % 4 (32 output rows) and every
+// second 128-byte column chunk (w / 4); it converts its 32 x CPC block into a private SW128
+// staging buffer (two 4 KB buffers, alternating) and its lane 0 issues the TMA store of a
+// (CPC x 32-row) box -- no CTA-wide barriers in the epilogue.
+template <int DT, class StoreFn>
+__device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0, int N, const EpiS& cs, const Epi& e,
+                                                   uint8_t* wstage, int& sbuf, StoreFn&& store) {
+  constexpr int ES = Tr<DT>::ES;
+  constexpr int CPC = 128 / ES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, h = warp >> 2;
+  const int valid = min(BN, N - n0);
+  const int nch = (valid + CPC - 1) / CPC;
+  for (int cc = h; cc < nch; cc += 2, ++sbuf) {
+    uint8_t* buf = wstage + (sbuf & 1) * 4096;
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+#pragma unroll 1
+    for (int c32 = 0; c32 < CPC; c32 += 32) {
+      const int c0 = cc * CPC + c32;
+      if (c0 >= BN) break;
+      uint32_t r[32];
+      tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t o[8];
+        epi16<DT>(&r[16 * hh], cs, e, n0 + c0 + 16 * hh, o);
+        const int vi0 = (c32 + 16 * hh) * ES / 16;
+#pragma unroll
+        for (int v = 0; v < ES; ++v)
+          sts128(smem_u32(buf) + sw128_vec(lane, vi0 + v), o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      store(buf, n0 + cc * CPC, q * 32);
+      bulk_commit();
+    }
+  }
+}
+
 // =====================================================================================
 // LBL PW: Y[M,N] = eps(X[M,K] . Wp[N,K]^T). Warps 0-7 epilogue, 8 TMA producer, 9 MMA.
 // =====================================================================================
@@ -153,8 +196,8 @@ __global__ void __launch_bounds__(320, 1)
   constexpr int KSTEP = 32 / Tr<DT>::ES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* stage = smem;                         // 2 x 16 KB output staging
-  uint8_t* abuf = smem + 32768;
+  uint8_t* stage = smem;                         // 8 warps x 2 x 4 KB output staging
+  uint8_t* abuf = smem + 65536;
   uint8_t* bbuf = abuf + stages * 16384;
   uint8_t* cst = bbuf + stages * BN * 128;
   uint64_t* full = reinterpret_cast<uint64_t*>(cst + consts_bytes<DT>(ncap));
@@ -234,13 +277,13 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(tfull + acc, (local >> 1) & 1);
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
-      epilogue_tile<DT, 8>(tbase + acc * BN, BN, n0, N, cs, ep, stage, sbuf,
-                           [&](const uint8_t* buf, int c) { tma_store_2d(&tmy, buf, c, m0); });
+      epilogue_tile_warp<DT>(tbase + acc * BN, BN, n0, N, cs, ep, stage + warp * 8192, sbuf,
+                             [&](const uint8_t* buf, int c, int r) { tma_store_2d(&tmy, buf, c, m0 + r); });
       tc_fence_before();
       mbar_arrive(tempty + acc);
       if (threadIdx.x == 0) stamp(local, 5);
     }
-    if (threadIdx.x == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
   }
   __syncthreads();
   if (warp == 9) {
@@ -796,7 +839,7 @@ static bool out_tmap_2d(CUtensorMap* m, int dt, void* y, int M, int N) {
   const int ES = elem_size(dt);
   const uint64_t dims[2] = {(uint64_t)N, (uint64_t)M};
   const uint64_t str[1] = {(uint64_t)N * ES};
-  const uint32_t box[2] = {(uint32_t)(128 / ES), 128};
+  const uint32_t box[2] = {(uint32_t)(128 / ES), 32};  // one warp's 32 rows
   return encode_tmap(m, tmap_dtype(dt), 2, y, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
@@ -823,7 +866,7 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   }
   if (!out_tmap_2d(&ty, DT, y, M, N)) return set_error(FCM_E_CUDA, "tensor map (PW Y) failed");
   const int ncap = round_up(nbn * BN, 16);
-  const int fixed = 1024 + 32768 + consts_bytes<DT>(ncap) + 256;
+  const int fixed = 1024 + 65536 + consts_bytes<DT>(ncap) + 256;
   const int stage_bytes = 16384 + BN * 128;
   const int budget = device_props().smem_optin - fixed;
   const int nk = (K + KC - 1) / KC;
