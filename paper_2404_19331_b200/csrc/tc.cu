@@ -143,7 +143,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tacc, int BN, int n0, int
 // second 128-byte column chunk (w / 4); it converts its 32 x CPC block into a private SW128
 // staging buffer (two 4 KB buffers, alternating) and its lane 0 issues the TMA store of a
 // (CPC x 32-row) box -- no CTA-wide barriers in the epilogue.
-template <int DT, class StoreFn>
+template <int DT, int G, class StoreFn>
 __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0, int N, const EpiS& cs, const Epi& e,
                                                    uint8_t* wstage, int& sbuf, StoreFn&& store) {
   constexpr int ES = Tr<DT>::ES;
@@ -152,9 +152,9 @@ __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0
   const int q = warp & 3, h = warp >> 2;
   const int valid = min(BN, N - n0);
   const int nch = (valid + CPC - 1) / CPC;
-  for (int cc = h; cc < nch; cc += 2, ++sbuf) {
-    uint8_t* buf = wstage + (sbuf & 1) * 4096;
-    if (lane == 0) bulk_wait_read<1>();
+  for (int cc = h; cc < nch; cc += G, ++sbuf) {
+    uint8_t* buf = wstage;  // one 4 KB buffer per warp: wait until its previous store has read it
+    if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
 #pragma unroll 1
     for (int c32 = 0; c32 < CPC; c32 += 32) {
@@ -186,51 +186,59 @@ __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0
 // LBL PW: Y[M,N] = eps(X[M,K] . Wp[N,K]^T). Warps 0-7 epilogue, 8 TMA producer, 9 MMA.
 // =====================================================================================
 template <int DT>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(576, 1)
     pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                  const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, int stages,
-                 uint32_t tmem_cols, int ncap, unsigned long long* trace) {
+                 uint32_t tmem_cols, int ncap, int resB, unsigned long long* trace, int dbg) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
   constexpr int KSTEP = 32 / Tr<DT>::ES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* stage = smem;                         // 8 warps x 2 x 4 KB output staging
+  uint8_t* stage = smem;                         // 16 warps x 4 KB output staging
   uint8_t* abuf = smem + 65536;
-  uint8_t* bbuf = abuf + stages * 16384;
-  uint8_t* cst = bbuf + stages * BN * 128;
+  uint8_t* bbuf = abuf + stages * 16384;         // resB: all nk chunks of this CTA's B slice, else a ring
+  const int nk = (K + KC - 1) / KC;
+  uint8_t* cst = bbuf + (resB ? nk : stages) * BN * 128;
   uint64_t* full = reinterpret_cast<uint64_t*>(cst + consts_bytes<DT>(ncap));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, N, ncap, cst);
-  if (warp == 8 && lane == 0) {
+  if (warp == 16 && lane == 0) {
     tma_prefetch_desc(&tma);
     tma_prefetch_desc(&tmb);
     tma_prefetch_desc(&tmy);
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 256); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 512); }
+    mbar_init(bfull, 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc_rt(tslot, tmem_cols);
+  if (warp == 17) tmem_alloc_rt(tslot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const int nk = (K + KC - 1) / KC;
   const int nbm = (M + 127) / 128;
   const int total = nbm * nbn;
-  const uint32_t stage_tx = 16384 + BN * 128;
   auto stamp = [&](int local, int ev) {
     if (trace && blockIdx.x == 0 && local < 64) trace[local * 16 + ev] = clock64();
   };
 
-  if (warp == 8) {
+  if (warp == 16) {
     if (lane == 0) {
       int it = 0, lt = 0;
+      if (resB) {
+        // the grid is a multiple of nbn, so this CTA's C_out slice never changes: load it once
+        // (a per-tile reload has every SM re-reading the same few KB of L2 each tile)
+        mbar_arrive_expect_tx(bfull, nk * BN * 128);
+        for (int kc = 0; kc < nk; ++kc)
+          tma_load_2d(bbuf + kc * BN * 128, &tmb, bfull, kc * KC, (blockIdx.x % nbn) * BN);
+      }
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
         const int m0 = (t / nbn) * 128, n0 = (t % nbn) * BN;
         for (int kc = 0; kc < nk; ++kc, ++it) {
@@ -238,16 +246,17 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(empty + s, ph ^ 1);
           if (kc == 0) stamp(lt, 8);
-          mbar_arrive_expect_tx(full + s, stage_tx);
+          mbar_arrive_expect_tx(full + s, 16384 + (resB ? 0 : BN * 128));
           tma_load_2d(abuf + s * 16384, &tma, full + s, kc * KC, m0);
-          tma_load_2d(bbuf + s * BN * 128, &tmb, full + s, kc * KC, n0);
+          if (!resB) tma_load_2d(bbuf + s * BN * 128, &tmb, full + s, kc * KC, n0);
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, BN);
       int it = 0, local = 0;
+      if (resB) mbar_wait(bfull, 0);
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local & 1;
         mbar_wait(tempty + acc, ((local >> 1) & 1) ^ 1);
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(320, 1)
           if (kc == 0) stamp(local, 1);
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(abuf + s * 16384));
-          const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + s * BN * 128));
+          const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + (resB ? kc : s) * BN * 128));
           const int ksteps = min(4, (K - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
           for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
           mma_commit(empty + s);
@@ -277,8 +286,11 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(tfull + acc, (local >> 1) & 1);
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
-      epilogue_tile_warp<DT>(tbase + acc * BN, BN, n0, N, cs, ep, stage + warp * 8192, sbuf,
-                             [&](const uint8_t* buf, int c, int r) { tma_store_2d(&tmy, buf, c, m0 + r); });
+      if (!(dbg & 32))
+        epilogue_tile_warp<DT, 4>(tbase + acc * BN, BN, n0, N, cs, ep, stage + warp * 4096, sbuf,
+                                  [&](const uint8_t* buf, int c, int r) {
+                                    if (!(dbg & 16)) tma_store_2d(&tmy, buf, c, m0 + r);
+                                  });
       tc_fence_before();
       mbar_arrive(tempty + acc);
       if (threadIdx.x == 0) stamp(local, 5);
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) bulk_wait_all();
   }
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 17) {
     tc_fence_after();
     tmem_dealloc_rt(tbase, tmem_cols);
   }
@@ -790,6 +802,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
 
 // ------------------------------------------------------------------------------- launchers
 // FCM_DEBUG_FLAGS (env, development only): bit 0 skip DW math, bit 1 skip PW epilogue, bit 2 DW
+// (bits 4/5: LBL PW skips its TMA store / its whole epilogue)
 // warps do not wait for the TMA. Results are wrong when set; used to attribute time to roles.
 static int debug_flags() {
   static int f = [] { const char* e = getenv("FCM_DEBUG_FLAGS"); return e ? atoi(e) : 0; }();
@@ -867,17 +880,30 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   if (!out_tmap_2d(&ty, DT, y, M, N)) return set_error(FCM_E_CUDA, "tensor map (PW Y) failed");
   const int ncap = round_up(nbn * BN, 16);
   const int fixed = 1024 + 65536 + consts_bytes<DT>(ncap) + 256;
-  const int stage_bytes = 16384 + BN * 128;
   const int budget = device_props().smem_optin - fixed;
   const int nk = (K + KC - 1) / KC;
-  int stages = std::min(std::max(2 * nk, 4), std::min(8, budget / stage_bytes));
-  if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pw: not enough shared memory for 2 stages");
-  const size_t smem = (size_t)fixed + (size_t)stages * stage_bytes;
+  const int total = ((M + 127) / 128) * nbn;
+  int grid = std::min(total, device_props().sms);
+  // resident B: the CTA keeps its whole C_out slice of the weights in smem (grid a multiple of nbn
+  // so the slice is fixed) when that still leaves >= 4 A stages
+  const int resgrid = (grid / nbn) * nbn;
+  const bool resB = resgrid > 0 && budget - nk * BN * 128 >= 4 * 16384 && resgrid >= grid * 15 / 16;
+  int stages;
+  size_t smem;
+  if (resB) {
+    grid = resgrid;
+    stages = std::min(std::max(2 * nk, 4), std::min(8, (budget - nk * BN * 128) / 16384));
+    smem = (size_t)fixed + (size_t)stages * 16384 + (size_t)nk * BN * 128;
+  } else {
+    const int stage_bytes = 16384 + BN * 128;
+    stages = std::min(std::max(2 * nk, 4), std::min(8, budget / stage_bytes));
+    if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pw: not enough shared memory for 2 stages");
+    smem = (size_t)fixed + (size_t)stages * stage_bytes;
+  }
   auto kern = pw_tc_kernel<DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int total = ((M + 127) / 128) * nbn;
-  const int grid = std::min(total, device_props().sms);
-  kern<<<grid, 320, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, stages, pow2_cols(2 * BN), ncap, trace_buf());
+  kern<<<grid, 576, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, stages, pow2_cols(2 * BN), ncap, resB ? 1 : 0,
+                                trace_buf(), debug_flags());
   const int rc = check_launch("pw_tc_kernel");
   trace_dump("pw");
   return rc;

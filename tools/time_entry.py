@@ -15,8 +15,10 @@ ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--entries", default="22")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--plan-file", default="")
 a = ap.parse_args()
-plan = fcm.plan(model_json(a.net, a.dtype, a.batch))
+import json  # noqa: E402
+plan = json.load(open(a.plan_file)) if a.plan_file else fcm.plan(model_json(a.net, a.dtype, a.batch))
 netw = Network(a.net, a.dtype, a.batch, plan)
 ids = list(range(len(netw.steps))) if a.entries == "all" else [int(i) for i in a.entries.split(",")]
 for i in ids:
