@@ -319,7 +319,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
     dwpw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                    const __grid_constant__ CUtensorMap tmy, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
                    Epi ep, int N, int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw,
-                   int tiles_x, int tiles_y, int nsplit, int BN, int XS, int BS, uint32_t tmem_cols, int ncap, int dbg) {
+                   int tiles_x, int tiles_y, int nsplit, int BN, int XS, int BS, uint32_t tmem_cols, int ncap, int resB,
+                   int dbg) {
   constexpr int V = Tr<DT>::VEC;
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   uint8_t* ostage = smem;                        // 2 x 16 KB output staging
   uint8_t* abuf = smem + 32768;                  // kDwpwNA x 16 KB A operand (commBuffer) ring
   uint8_t* xbuf = abuf + kDwpwNA * 16384;        // XS x X halo chunks (TMA -> DW)
-  uint8_t* bbuf = xbuf + XS * xstride;           // BS x PW weight chunks (TMA -> MMA)
+  uint8_t* bbuf = xbuf + XS * xstride;           // BS x PW weight chunks (TMA -> MMA); resB: BS = nk, loaded once
   uint8_t* cst = bbuf + BS * BN * 128;
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(nk * KC));  // DW weights
@@ -397,7 +398,13 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   } else if (warp == WARP_TB) {
     if (lane == 0) {
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      if (resB) {  // grid is a multiple of nsplit: this CTA's C_out slice is fixed
+        for (int kc = 0; kc < nk; ++kc) {
+          mbar_arrive_expect_tx(fullB + kc, BN * 128);
+          tma_load_2d(bbuf + kc * BN * 128, &tmb, fullB + kc, kc * KC, (blockIdx.x % nsplit) * BN);
+        }
+      }
+      for (int t = blockIdx.x; t < total && !resB; t += gridDim.x) {
         const int ns = t % nsplit;
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % BS;
@@ -417,16 +424,16 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
         tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int a = it % kDwpwNA, sb = it % BS;
+          const int a = it % kDwpwNA, sb = resB ? kc : it % BS;
           mbar_wait(afull + a, (it / kDwpwNA) & 1);
-          mbar_wait(fullB + sb, (it / BS) & 1);
+          mbar_wait(fullB + sb, resB ? 0 : (it / BS) & 1);
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(abuf + a * 16384));
           const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + sb * BN * 128));
           const int ksteps = min(4, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
           for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
           mma_commit(aempty + a);
-          mma_commit(emptyB + sb);
+          if (!resB) mma_commit(emptyB + sb);
         }
         mma_commit(tfull + acc);
       }
@@ -559,7 +566,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     pwdw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                    const typename Tr<DT>::T* __restrict__ wdw, Epi ep, Epi ed, uint8_t* __restrict__ y, int N, int H,
                    int W, int Cin, int Ho, int Wo, int Cmid, int pt, int pl, int nb, int th, int tw, int tiles_x,
-                   int tiles_y, int stages, int depth, uint32_t tmem_cols, int ncap, int dbg,
+                   int tiles_y, int stages, int depth, uint32_t tmem_cols, int ncap, int resB, int dbg,
                    unsigned long long* trace) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int V = Tr<DT>::VEC;
@@ -576,13 +583,15 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   const int MB = (R + 127) / 128;
   const int xbytes = R * 128;
   const int astride = MB * 16384;
-  const int stage_bytes = astride + TD * 128;
+  const int stage_bytes = astride + (resB ? 0 : TD * 128);
   const int tbytes = ((R * PITCH) + 1023) & ~1023;
   const int nslice = (Cmid + TD - 1) / TD;
+  const int nk = (Cin + KC - 1) / KC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* tsm = smem + stages * stage_bytes;  // `depth` T buffers
-  uint8_t* cst = tsm + depth * tbytes;
+  uint8_t* bres = tsm + depth * tbytes;        // resB: this CTA's PW weight slice, all nk chunks
+  uint8_t* cst = bres + (resB ? nk * TD * 128 : 0);
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(ncap));
   uint64_t* full = reinterpret_cast<uint64_t*>(wsm + K * K * nslice * 32);
@@ -591,7 +600,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   uint64_t* tempty = tfull + 4;
   uint64_t* Tfull = tempty + 4;
   uint64_t* Tempty = Tfull + 4;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(Tempty + 4);
+  uint64_t* bfull = Tempty + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cmid, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cmid, ncap, dcst);
@@ -606,6 +616,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       mbar_init(Tfull + a, NTP * 32);
       mbar_init(Tempty + a, kPwdwNDW * 32);
     }
+    mbar_init(bfull, 1);
     fence_barrier_init();
   }
   if (warp == WARP_MMA) tmem_alloc_rt(tslot, tmem_cols);
@@ -613,7 +624,6 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const int nk = (Cin + KC - 1) / KC;
   const int spatial = ((N + nb - 1) / nb) * tiles_y * tiles_x;
   const int total = spatial * nslice;
   const uint32_t acc_cols = MB * TD;
@@ -633,8 +643,13 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
 
   if (warp == WARP_TMA) {
     if (lane == 0) {
-      const uint32_t tx = xbytes + TD * 128;
+      const uint32_t tx = xbytes + (resB ? 0 : TD * 128);
       int it = 0;
+      if (resB) {  // grid is a multiple of nslice: this CTA's C_mid slice is fixed, load its weights once
+        mbar_arrive_expect_tx(bfull, nk * TD * 128);
+        for (int kc = 0; kc < nk; ++kc)
+          tma_load_2d(bres + kc * TD * 128, &tmb, bfull, kc * KC, (blockIdx.x % nslice) * TD);
+      }
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int sl, nbi, tyi, txi;
         decode(t, sl, nbi, tyi, txi);
@@ -649,7 +664,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
           }
           mbar_arrive_expect_tx(full + s, tx);
           tma_load_4d(st, &tmx, full + s, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
-          tma_load_2d(st + astride, &tmb, full + s, kc * KC, sl * TD);
+          if (!resB) tma_load_2d(st + astride, &tmb, full + s, kc * KC, sl * TD);
         }
       }
     }
@@ -657,6 +672,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     if (lane == 0) {
       const uint32_t idesc = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, TD);
       int it = 0, local = 0;
+      if (resB) mbar_wait(bfull, 0);
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local % depth;
         mbar_wait(tempty + acc, ((local / depth) & 1) ^ 1);
@@ -668,7 +684,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
           if (kc == 0) stamp(local, 1);
           tc_fence_after();
           uint8_t* st = smem + s * stage_bytes;
-          const uint64_t bd = smem_desc_sw128(smem_u32(st + astride));
+          const uint64_t bd = smem_desc_sw128(smem_u32(resB ? bres + kc * TD * 128 : st + astride));
           for (int mb = 0; mb < MB; ++mb) {
             const uint64_t ad = smem_desc_sw128(smem_u32(st + mb * 16384));
             const uint32_t d = tbase + acc * acc_cols + mb * TD;
@@ -954,21 +970,30 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   const int nk = (g.C + KC - 1) / KC;
   const int fixed = 1024 + 32768 + kDwpwNA * 16384 + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + K * K * nk * 128 + 512;
   const int xstride = ((g.nb * th_in * tw_in * 128) + 1023) & ~1023;
-  const int BS = 2;
-  const int budget = device_props().smem_optin - fixed - BS * BN * 128;
-  const int XS = std::min(6, budget / xstride);
+  const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
+  const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
+  int grid = std::min(total, device_props().sms);
+  int BS = 2;
+  int XS = std::min(6, (device_props().smem_optin - fixed - BS * BN * 128) / xstride);
   if (XS < 2) return set_error(FCM_E_INFEASIBLE, "dwpw: tile too large for 2 X stages");
+  // resident weights: grid a multiple of nsplit fixes each CTA's C_out slice; keep all nk chunks
+  // when that costs at most one X stage (and leaves >= 2)
+  const int resgrid = (grid / nsplit) * nsplit;
+  const int xs_res = std::min(6, (device_props().smem_optin - fixed - nk * BN * 128) / xstride);
+  const bool resB = nk <= 16 && resgrid > 0 && resgrid >= grid * 15 / 16 && xs_res >= 2 && xs_res >= XS - 1;
+  if (resB) {
+    grid = resgrid;
+    BS = nk;
+    XS = xs_res;
+  }
   const size_t smem = (size_t)fixed + (size_t)BS * BN * 128 + (size_t)XS * xstride;
   auto kern = dwpw_tc_kernel<DT, K, S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
-  const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
-  const int grid = std::min(total, device_props().sms);
   using TT = typename Tr<DT>::T;
   kern<<<grid, (4 + dwpw_ndw<DT, K>() + 3) * 32, smem, st>>>(tx, tb, ty, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
                                                               g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw,
                                                               tiles_x, tiles_y, nsplit, BN, XS, BS, pow2_cols(2 * BN),
-                                                              ncap, debug_flags());
+                                                              ncap, resB ? 1 : 0, debug_flags());
   return check_launch("dwpw_tc_kernel");
 }
 
@@ -1017,29 +1042,45 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
     if (!encode_tmap(&tb, tmap_dtype(DT), 2, wp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return set_error(FCM_E_CUDA, "tensor map (PWDW B) failed");
   }
-  const int stage_bytes = MB * 16384 + TD * 128;
   const int tbytes = ((R * (128 + 16)) + 1023) & ~1023;
   const int ncap = round_up(g.Cout, TD);
   const int nslice = ncap / TD;
+  const int nk = (g.C + KC - 1) / KC;
   const int depth = std::min(3, 512 / (MB * TD));  // TMEM accumulators = T buffers in flight
   const int fixed = 1024 + 2 * consts_bytes<DT>(ncap) + K * K * nslice * 128 + 512;
-  int stages = 0, dep = depth;
-  for (; dep >= 2; --dep) {
-    stages = std::min(4, (device_props().smem_optin - fixed - dep * tbytes) / stage_bytes);
-    if (stages >= 2) break;
-  }
-  if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pwdw_r: tile too large for 2 smem stages");
-  const size_t smem = (size_t)fixed + (size_t)dep * tbytes + (size_t)stages * stage_bytes;
-  auto kern = pwdw_tc_kernel<DT, K, S>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nslice;
-  const int grid = std::min(total, device_props().sms);
+  int grid = std::min(total, device_props().sms);
+  // resident weights (as in the LBL PW): with the grid a multiple of nslice each CTA's C_mid slice
+  // is fixed, so its nk weight chunks are loaded once instead of once per tile by every CTA
+  auto plan = [&](bool res, int& stages, int& dep) {
+    const int sb = MB * 16384 + (res ? 0 : TD * 128), extra = res ? nk * TD * 128 : 0;
+    for (dep = depth; dep >= 2; --dep) {
+      stages = std::min(4, (device_props().smem_optin - fixed - extra - dep * tbytes) / sb);
+      if (stages >= 2) return (size_t)fixed + extra + (size_t)dep * tbytes + (size_t)stages * sb;
+    }
+    stages = 0;
+    return (size_t)0;
+  };
+  int stages = 0, dep = 0;
+  const int resgrid = (grid / nslice) * nslice;
+  bool resB = resgrid > 0 && resgrid >= grid * 15 / 16;
+  size_t smem = resB ? plan(true, stages, dep) : 0;
+  if (resB && stages >= 2) {
+    grid = resgrid;
+  } else {
+    resB = false;
+    smem = plan(false, stages, dep);
+  }
+  if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pwdw_r: tile too large for 2 smem stages");
+  auto kern = pwdw_tc_kernel<DT, K, S>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   using TT = typename Tr<DT>::T;
   kern<<<grid, (pwdw_ntp<K>() + kPwdwNDW + 2) * 32, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ep, ed,
                                                      static_cast<uint8_t*>(y), g.N, g.H, g.W, g.C, g.Ho, g.Wo, g.Cout,
                                                      g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages, dep,
-                                                     pow2_cols(dep * MB * TD), ncap, debug_flags(), trace_buf());
+                                                     pow2_cols(dep * MB * TD), ncap, resB ? 1 : 0, debug_flags(),
+                                                     trace_buf());
   const int rc = check_launch("pwdw_tc_kernel");
   trace_dump("pwdw");
   return rc;
