@@ -402,20 +402,46 @@ __device__ __forceinline__ void dw_segh(uint32_t src, int col_bytes, int row_byt
   }
 }
 
-// Epilogue of an fp32 pair -> packed bf16x2 / f16x2 word (scale/bias as pairs, clamp = activation).
+// Division by a runtime-invariant divisor d >= 1 without the ~15-instruction integer divide:
+// q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1 (exact for
+// 0 <= n < 2^31). The magic pair is computed on the host and passed as a kernel parameter.
+struct FDiv {
+  uint32_t m, l;
+};
+inline FDiv make_fdiv(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  return FDiv{static_cast<uint32_t>(((1ull << 32) * ((1ull << l) - d)) / d + 1), l};
+}
+__device__ __forceinline__ int fdiv(int n, FDiv f) {
+  return static_cast<int>((__umulhi(static_cast<uint32_t>(n), f.m) + static_cast<uint32_t>(n)) >> f.l);
+}
+
+// Activation bounds as a packed pair (both halves = the bound, rounded to DT; all three bounds
+// -inf / 0 / 6 / +inf are exact in bf16 and f16).
 template <int DT>
-__device__ __forceinline__ uint32_t epi2_pack(uint64_t acc, uint64_t sc, uint64_t bi, float lo_c, float hi_c) {
+__device__ __forceinline__ uint32_t bound2(float v) {
+  uint32_t h;
+  if constexpr (DT == FCM_BF16) asm("cvt.rn.bf16x2.f32 %0, %1, %1;" : "=r"(h) : "f"(v));
+  else asm("cvt.rn.f16x2.f32 %0, %1, %1;" : "=r"(h) : "f"(v));
+  return h;
+}
+
+// Epilogue of an fp32 pair -> packed bf16x2 / f16x2 word (scale/bias as pairs, then the activation
+// clamp on the packed result: rounding is monotonic and the bounds are representable, so
+// clamp(round(v)) == round(clamp(v)) -- two packed min/max instead of four fp32 ones).
+template <int DT>
+__device__ __forceinline__ uint32_t epi2_pack(uint64_t acc, uint64_t sc, uint64_t bi, uint32_t lo2, uint32_t hi2) {
   float a, b;
   f2_unpack(f2_fma(acc, sc, bi), a, b);
-  a = fminf(fmaxf(a, lo_c), hi_c);
-  b = fminf(fmaxf(b, lo_c), hi_c);
-  if constexpr (DT == FCM_BF16) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  } else {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
+  uint32_t h;
+  if constexpr (DT == FCM_BF16)
+    asm("{cvt.rn.bf16x2.f32 %0, %2, %1;\n\tmax.bf16x2 %0, %0, %3;\n\tmin.bf16x2 %0, %0, %4;}"
+        : "=r"(h) : "f"(a), "f"(b), "r"(lo2), "r"(hi2));
+  else
+    asm("{cvt.rn.f16x2.f32 %0, %2, %1;\n\tmax.f16x2 %0, %0, %3;\n\tmin.f16x2 %0, %0, %4;}"
+        : "=r"(h) : "f"(a), "f"(b), "r"(lo2), "r"(hi2));
+  return h;
 }
 
 // Load this lane's DW weights from a shared-memory copy of Wdw laid out [k*k][C/VEC words].

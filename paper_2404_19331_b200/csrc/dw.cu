@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     load_dw_weights_h<K>(W2, wdw, C, cval ? cl : C);
     const uint64_t sc2 = f2_pack(cval ? (ep.scale ? ep.scale[cl] : 1.f) : 0.f, cval ? (ep.scale ? ep.scale[cl + 1] : 1.f) : 0.f);
     const uint64_t bi2 = f2_pack(cval && ep.bias ? ep.bias[cl] : 0.f, cval && ep.bias ? ep.bias[cl + 1] : 0.f);
-    const float lo_c = act_lo(ep.act), hi_c = act_hi(ep.act);
+    const uint32_t lo_c = bound2<DT>(act_lo(ep.act)), hi_c = bound2<DT>(act_hi(ep.act));
     mbar_wait(&bar, 0);
     const int nseg = (nrows + kSeg - 1) / kSeg;
     const int ncolg = (tw + npix - 1) / npix;

@@ -313,6 +313,9 @@ __global__ void __launch_bounds__(576, 1)
 // DW warps per DWPW CTA: 16 for the paired-FP32 bf16/f16 3x3 core (fits 93 registers), else 8.
 template <int DT, int K> constexpr int dwpw_ndw() { return 8; }
 constexpr int kDwpwNA = 2;  // A-operand (commBuffer) ring depth
+struct DwDivs {
+  FDiv tw, n16, n8, n4;  // divisors tw and ceil(th / SEG) for SEG = 16, 8, 4
+};
 
 template <int DT, int K, int S>
 __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
                    const __grid_constant__ CUtensorMap tmy, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
                    Epi ep, int N, int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw,
                    int tiles_x, int tiles_y, int nsplit, int BN, int XS, int BS, uint32_t tmem_cols, int ncap, int resB,
-                   int dbg) {
+                   DwDivs dv, int dbg) {
   constexpr int V = Tr<DT>::VEC;
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
@@ -341,7 +344,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   uint8_t* cst = bbuf + BS * BN * 128;
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(nk * KC));  // DW weights
-  uint64_t* fullX = reinterpret_cast<uint64_t*>(wsm + K * K * nk * 32);
+  uint8_t* dscr = reinterpret_cast<uint8_t*>(wsm + K * K * nk * 32);  // DW warps' dead-row scratch
+  uint64_t* fullX = reinterpret_cast<uint64_t*>(dscr + kDwpwNDW * 128);
   uint64_t* emptyX = fullX + XS;
   uint64_t* fullB = emptyX + XS;
   uint64_t* emptyB = fullB + BS;
@@ -446,6 +450,10 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
+    const uint32_t lo_c = bound2<DT>(act_lo(ed.act)), hi_c = bound2<DT>(act_hi(ed.act));
+    DwWh<K> W2;
+    uint64_t sc2 = 0, bi2 = 0;
+    int kc_w = -1;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       for (int kc = 0; kc < nk; ++kc, ++it) {
@@ -455,48 +463,49 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
         const uint32_t abase = smem_u32(abuf + a * 16384);
         if constexpr (kPair) {
           // lane groups: a partially filled chunk (C_in not a multiple of 64) packs 2 or 4 output
-          // columns into one warp (gs lanes per pixel) instead of idling the empty lanes
-          const int cw_valid = min(32, (Cin - kc * KC) / V);
-          const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
-          const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
-          const int cl = kc * KC + wd * V;
-          DwWh<K> W2;
-          load_dw_weights_h_smem<K>(W2, wsm, nk * 32, kc * 32 + wd);
-          const uint64_t sc2 = f2_pack(dcs.sc(cl), dcs.sc(cl + 1)), bi2 = f2_pack(dcs.bi(cl), dcs.bi(cl + 1));
+          // columns into one warp (gs = 2^gsl lanes per pixel) instead of idling the empty lanes
+          const int cw_valid = min(32, (Cin - kc * KC) >> 1);
+          const int gsl = cw_valid > 16 ? 5 : (cw_valid > 8 ? 4 : 3);
+          const int npl = 5 - gsl;
+          const int grp = lane >> gsl, wd = lane & ((1 << gsl) - 1);
+          if (kc != kc_w) {  // weights / constants of this chunk (loaded once when nk == 1)
+            const int cl = kc * KC + wd * V;
+            load_dw_weights_h_smem<K>(W2, wsm, nk * 32, kc * 32 + wd);
+            sc2 = f2_pack(dcs.sc(cl), dcs.sc(cl + 1));
+            bi2 = f2_pack(dcs.bi(cl), dcs.bi(cl + 1));
+            kc_w = kc;
+          }
           const bool cval = wd < cw_valid;
-          const float lo_c = act_lo(ed.act), hi_c = act_hi(ed.act);
-          const int ncolg = (nb * tw + npix - 1) / npix;
-          const int nitems_g = ncolg * nseg;
+          const int ncg = (nb * tw + (1 << npl) - 1) >> npl;
+          const uint32_t dead = smem_u32(dscr) + (dw * 32 + lane) * 4;
           mbar_wait(fullX + sx, (it / XS) & 1);
           mbar_wait(aempty + a, ((it / kDwpwNA) & 1) ^ 1);
-          // segment length adapted to the tile height (compile-time per variant)
-          auto run_items = [&](auto segc) {
+          // segment length adapted to the tile height (compile-time per variant); item -> (column
+          // group, segment) and column -> (image, x) use host-computed magic divisors
+          auto run_items = [&](auto segc, FDiv fnsg) {
             constexpr int SEG = decltype(segc)::value;
             const int nsg = (th + SEG - 1) / SEG;
-            const int ncg = (gs == 32) ? nb * tw : ncolg;
             for (int item = dw; item < ncg * nsg && !(dbg & 1); item += kDwpwNDW) {
-              const int cg = item / nsg, seg = item - cg * nsg;
-              const int colr = (gs == 32) ? cg : cg * npix + grp;
+              const int cg = fdiv(item, fnsg), seg = item - cg * nsg;
+              const int colr = (cg << npl) + grp;
               const bool live = colr < nb * tw;
               const int col = live ? colr : 0;
-              const int b = col / tw, x = col - b * tw;
+              const int b = fdiv(col, dv.tw), x = col - b * tw;
               const int y0 = seg * SEG;
               const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + wd) * 4;
               const int mbase = (b * th + y0) * tw + x;
               const int nvalid = live ? th - y0 : 0;
               dw_segh<DT, K, S, SEG>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
-                if (r < nvalid) {
-                  const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
-                  sts32(abase + sw128_off(mbase + r * tw, wd), word);
-                }
+                // rows past the tile go to a per-lane scratch word: a select, not a branch
+                const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
+                sts32(r < nvalid ? abase + sw128_off(mbase + r * tw, wd) : dead, word);
               });
             }
           };
           // longest segment that still gives every DW warp an item (fewer window reloads)
-          const int ncg_ = (gs == 32) ? nb * tw : ncolg;
-          if (S == 1 && th > 8 && ncg_ * ((th + 15) / 16) >= kDwpwNDW) run_items(std::integral_constant<int, 16>());
-          else if (th > 4 && ncg_ * ((th + 7) / 8) >= kDwpwNDW / 2) run_items(std::integral_constant<int, 8>());
-          else run_items(std::integral_constant<int, 4>());
+          if (S == 1 && th > 8 && ncg * ((th + 15) / 16) >= kDwpwNDW) run_items(std::integral_constant<int, 16>(), dv.n16);
+          else if (th > 4 && ncg * ((th + 7) / 8) >= kDwpwNDW / 2) run_items(std::integral_constant<int, 8>(), dv.n8);
+          else run_items(std::integral_constant<int, 4>(), dv.n4);
         } else {
           DwW<DT, K> W;
           load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + lane);
@@ -750,7 +759,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     const int dw = warp - NTP;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
-    const float lo_c = act_lo(ed.act), hi_c = act_hi(ed.act);
+    const uint32_t lo_c = bound2<DT>(act_lo(ed.act)), hi_c = bound2<DT>(act_hi(ed.act));
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -968,7 +977,8 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   }
   const int ncap = round_up(nsplit * BN, 16);
   const int nk = (g.C + KC - 1) / KC;
-  const int fixed = 1024 + 32768 + kDwpwNA * 16384 + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + K * K * nk * 128 + 512;
+  const int fixed = 1024 + 32768 + kDwpwNA * 16384 + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + K * K * nk * 128 +
+                    dwpw_ndw<DT, K>() * 128 + 512;
   const int xstride = ((g.nb * th_in * tw_in * 128) + 1023) & ~1023;
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
@@ -993,7 +1003,10 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   kern<<<grid, (4 + dwpw_ndw<DT, K>() + 3) * 32, smem, st>>>(tx, tb, ty, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
                                                               g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw,
                                                               tiles_x, tiles_y, nsplit, BN, XS, BS, pow2_cols(2 * BN),
-                                                              ncap, resB ? 1 : 0, debug_flags());
+                                                              ncap, resB ? 1 : 0,
+                                                              DwDivs{make_fdiv(g.tw), make_fdiv((g.th + 15) / 16),
+                                                                     make_fdiv((g.th + 7) / 8), make_fdiv((g.th + 3) / 4)},
+                                                              debug_flags());
   return check_launch("dwpw_tc_kernel");
 }
 

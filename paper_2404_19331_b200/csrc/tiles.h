@@ -42,7 +42,7 @@ inline bool dwpw_tile_ok(const Geo& g, int nb, int th, int tw) {
   // mirror of launch_dwpw_t's layout: staging 32K + A ring 2x16K + B ring 2x(BN<=256)x128
   // + constants / DW weights (<= 24K) + at least 2 X stages
   const int xstride = ((nb * th_in * tw_in * 128) + 1023) & ~1023;
-  return 1024 + 32768 + 2 * 16384 + 2 * 256 * 128 + 24576 + 512 + 2 * xstride <= 232448;
+  return 1024 + 32768 + 2 * 16384 + 2 * 256 * 128 + 24576 + 1536 + 2 * xstride <= 232448;
 }
 
 inline void default_dwpw_tile(Geo& g) {
