@@ -569,14 +569,21 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
 constexpr int kPwdwNDW = 8;
 // T-producer warps (TMEM -> T): 8 (two per TMEM lane quadrant) for 3x3, 4 for 5x5 (registers).
 template <int K> constexpr int pwdw_ntp() { return K == 3 ? 8 : 4; }
+// rows per DW item of the PWDW_R consumers (must match kSeg in the kernel)
+template <int DT, int K, int S> constexpr int pwdw_seg() {
+  return ((DT == FCM_BF16 || DT == FCM_F16) && K == 3) ? (S == 1 ? 16 : 8) : 8;
+}
+struct PwdwDivs {
+  FDiv nslice, tx, ty, tw, nseg;  // tile decode + DW item decode
+};
 
 template <int DT, int K, int S>
 __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     pwdw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                    const typename Tr<DT>::T* __restrict__ wdw, Epi ep, Epi ed, uint8_t* __restrict__ y, int N, int H,
                    int W, int Cin, int Ho, int Wo, int Cmid, int pt, int pl, int nb, int th, int tw, int tiles_x,
-                   int tiles_y, int stages, int depth, uint32_t tmem_cols, int ncap, int resB, int dbg,
-                   unsigned long long* trace) {
+                   int tiles_y, int stages, int depth, uint32_t tmem_cols, int ncap, int resB, PwdwDivs dv,
+                   int dbg, unsigned long long* trace) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int V = Tr<DT>::VEC;
   constexpr int KC = 128 / ES;
@@ -642,12 +649,12 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     if (trace && blockIdx.x == 0 && local < 64) trace[local * 16 + ev] = clock64();
   };
   auto decode = [&](int t, int& sl, int& nbi, int& tyi, int& txi) {
-    sl = t % nslice;
-    int sp = t / nslice;
-    txi = sp % tiles_x;
-    sp /= tiles_x;
-    tyi = sp % tiles_y;
-    nbi = sp / tiles_y;
+    int sp = fdiv(t, dv.nslice);
+    sl = t - sp * nslice;
+    int q = fdiv(sp, dv.tx);
+    txi = sp - q * tiles_x;
+    nbi = fdiv(q, dv.ty);
+    tyi = q - nbi * tiles_y;
   };
 
   if (warp == WARP_TMA) {
@@ -755,12 +762,15 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   } else {
     // ---------------- DW consumers: T tile -> DW -> eps_dw -> OFM (128 B per warp store)
     constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
-    constexpr int kSeg = kPair ? (S == 1 ? 16 : 8) : 8;
+    constexpr int kSeg = pwdw_seg<DT, K, S>();
     const int dw = warp - NTP;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
     const uint32_t lo_c = bound2<DT>(act_lo(ed.act)), hi_c = bound2<DT>(act_hi(ed.act));
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
+    DwWh<K> W2;
+    uint64_t sc2 = 0, bi2 = 0;
+    int sl_w = -1;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int tbi = local % depth;
@@ -771,15 +781,18 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       const int y0t = tyi * th;
       const int nrows_t = min(th, Ho - y0t);
       if constexpr (kPair) {
-        DwWh<K> W2;
-        load_dw_weights_h_smem<K>(W2, wsm, nslice * 32, sl * 32 + lane);
-        const uint64_t sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1)), bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
+        if (sl != sl_w) {  // this slice's weights / constants (once per CTA with resident slices)
+          load_dw_weights_h_smem<K>(W2, wsm, nslice * 32, sl * 32 + lane);
+          sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1));
+          bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
+          sl_w = sl;
+        }
         const bool cval = c < Cmid;
         mbar_wait(Tfull + tbi, (local / depth) & 1);
         if (dw == 0 && lane == 0) stamp(local, 6);
         for (int item = dw; item < nitems && !(dbg & 1); item += kPwdwNDW) {
-          const int col = item / nseg, seg = item - col * nseg;
-          const int b = col / tw, x = col - b * tw;
+          const int col = fdiv(item, dv.nseg), seg = item - col * nseg;
+          const int b = fdiv(col, dv.tw), x = col - b * tw;
           const int n = nbi * nb + b, xo = txi * tw + x;
           const int y0 = seg * kSeg;
           if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
@@ -788,7 +801,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
           uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
           const size_t rstride = (size_t)Wo * Cmid / V;
           dw_segh<DT, K, S, kSeg>(src, PITCH, tw_in * PITCH, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
-            if (r < nvalid && cval) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
+            const uint32_t word = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
+            if (r < nvalid && cval) dst[r * rstride] = word;  // predicated store, no branch
           });
         }
       } else {
@@ -799,8 +813,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
         for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
         mbar_wait(Tfull + tbi, (local / depth) & 1);
         for (int item = dw; item < nitems; item += kPwdwNDW) {
-          const int col = item / nseg, seg = item - col * nseg;
-          const int b = col / tw, x = col - b * tw;
+          const int col = fdiv(item, dv.nseg), seg = item - col * nseg;
+          const int b = fdiv(col, dv.tw), x = col - b * tw;
           const int n = nbi * nb + b, xo = txi * tw + x;
           const int y0 = seg * kSeg;
           if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
@@ -1092,8 +1106,12 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   kern<<<grid, (pwdw_ntp<K>() + kPwdwNDW + 2) * 32, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ep, ed,
                                                      static_cast<uint8_t*>(y), g.N, g.H, g.W, g.C, g.Ho, g.Wo, g.Cout,
                                                      g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages, dep,
-                                                     pow2_cols(dep * MB * TD), ncap, resB ? 1 : 0, debug_flags(),
-                                                     trace_buf());
+                                                     pow2_cols(dep * MB * TD), ncap, resB ? 1 : 0,
+                                                     PwdwDivs{make_fdiv(nslice), make_fdiv(tiles_x), make_fdiv(tiles_y),
+                                                              make_fdiv(g.tw),
+                                                              make_fdiv((g.th + pwdw_seg<DT, K, S>() - 1) /
+                                                                        pwdw_seg<DT, K, S>())},
+                                                     debug_flags(), trace_buf());
   const int rc = check_launch("pwdw_tc_kernel");
   trace_dump("pwdw");
   return rc;
