@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfcm.so")
+LIB_PATH = os.environ.get("FCM_LIB_PATH") or os.path.join(_HERE, "libfcm.so")  # override: dev experiments
 
 FCM_OK, FCM_E_INVAL, FCM_E_ALIGN, FCM_E_UNSUPPORTED, FCM_E_INFEASIBLE, FCM_E_CUDA, FCM_E_BUFSZ = 0, -1, -2, -3, -4, -5, -6
 FCM_F32, FCM_BF16, FCM_F16, FCM_S8 = 0, 1, 2, 3

@@ -284,7 +284,11 @@ __device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
 template <int DT>
 __device__ __forceinline__ uint64_t word_to_f2(uint32_t w) {
   if constexpr (DT == FCM_BF16) {
-    return f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+    // two byte permutes (ALU pipe; `w << 16` would become an IMAD on the FMA pipe the FFMA2s use)
+    uint32_t lo, hi;
+    asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(lo) : "r"(w));
+    asm("prmt.b32 %0, %1, 0, 0x3244;" : "=r"(hi) : "r"(w));
+    return f2_pack(__uint_as_float(lo), __uint_as_float(hi));
   } else {
     __half2 h = *reinterpret_cast<__half2*>(&w);
     float2 f = __half22float2(h);
@@ -480,5 +484,132 @@ __device__ __forceinline__ void stage_dw_weights(const void* wdw, int k, int C, 
 __device__ __forceinline__ uint32_t sw128_off(int m, int wd) {
   return (m >> 3) * 1024 + (m & 7) * 128 + ((((wd >> 2) ^ (m & 7))) << 4) + ((wd & 3) << 2);
 }
+
+// ---------------------------------------------------------------------------- column-pair FFMA2 DW core
+// bf16 / f16, 3x3. A lane owns one 32-bit word (2 channels) of TWO adjacent output columns
+// (x0, x0+1) over SEG output rows. Input rows stream through once: each row's 3+S words are read
+// (ld.shared), widened to fp32 pairs, and fed as packed FFMA2 (fma.rn.f32x2, two IEEE fp32 FMAs
+// per instruction) into the <= 3 x 2 output accumulators that use the row. The folded-BN scale
+// is pre-multiplied into the fp32 weights and the accumulator starts at the bias (reading R3:
+// per-channel affine Norm), so the epilogue is the rounding + activation clamp only. Tap order
+// (i, j) is fixed: every kernel using this core gives bit-identical DW results.
+// Per output word: (3+S)((SEG-1)S+3)/(2 SEG) loads, 9 FFMA2, 1-2 packs.
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+
+template <int DT, int S, int SEG, class Sink>
+__device__ __forceinline__ void dw3_pair(uint32_t src, int col_bytes, int row_bytes, int y0, int max_row,
+                                         const uint64_t (&W)[9], uint64_t bias, Sink&& sink) {
+  constexpr int NCW = 3 + S;              // input words per row feeding 2 output columns
+  constexpr int WR = (SEG - 1) * S + 3;   // input rows of the segment
+  constexpr int PD = 2;                   // software pipelining: rows loaded ahead of their use
+  uint64_t acc[SEG][2];
+  uint32_t raw[WR][NCW];
+  auto load_row = [&](int ii) {
+    const uint32_t rp = src + min(y0 * S + ii, max_row) * row_bytes;
+#pragma unroll
+    for (int j = 0; j < NCW; ++j) raw[ii][j] = lds32(rp + j * col_bytes);
+  };
+#pragma unroll
+  for (int ii = 0; ii < PD && ii < WR; ++ii) load_row(ii);
+#pragma unroll
+  for (int ii = 0; ii < WR; ++ii) {
+    if (ii + PD < WR) load_row(ii + PD);
+    uint64_t x[NCW];
+#pragma unroll
+    for (int j = 0; j < NCW; ++j) x[j] = word_to_f2<DT>(raw[ii][j]);
+#pragma unroll
+    for (int r = 0; r < SEG; ++r) {
+      const int i = ii - r * S;  // kernel row of this input row for output row r
+      if (i < 0 || i > 2) continue;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          acc[r][c] = f2_fma(x[c * S + j], W[i * 3 + j], (i == 0 && j == 0) ? bias : acc[r][c]);
+      if (i == 2) sink(r, acc[r][0], acc[r][1]);
+    }
+  }
+}
+
+// fp32 pair -> packed bf16x2 / f16x2 with the activation: ACT 0 none, 1 relu (free in the
+// convert), 2 relu6 (relu convert + one packed min; 6 is exact in both formats).
+template <int DT, int ACT>
+__device__ __forceinline__ uint32_t pack_act(uint64_t acc, uint32_t hi2) {
+  float a, b;
+  f2_unpack(acc, a, b);
+  uint32_t h;
+  if constexpr (DT == FCM_BF16) {
+    if constexpr (ACT == 0) asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    else asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    if constexpr (ACT == 2) asm("min.bf16x2 %0, %0, %1;" : "+r"(h) : "r"(hi2));
+  } else {
+    if constexpr (ACT == 0) asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    else asm("cvt.rn.relu.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    if constexpr (ACT == 2) asm("min.f16x2 %0, %0, %1;" : "+r"(h) : "r"(hi2));
+  }
+  return h;
+}
+
+// Stage the 3x3 DW weights of C channels as scale-folded fp32 pairs [9][cwords] (uint64) plus the
+// bias pairs [cwords], zero past C. Both arrays are read back with ld.shared.u64 per lane.
+template <int DT>
+__device__ __forceinline__ void stage_dw3_f2(const void* wdw, const Epi& e, int C, int cwords, uint64_t* wsm2,
+                                             uint64_t* bsm2) {
+  const uint32_t* g = static_cast<const uint32_t*>(wdw);
+  const int cw_real = C / 2;
+  const int n = 10 * cwords;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int t = i / cwords, w = i - t * cwords;
+    const bool v = w < cw_real;
+    const float s0 = (v && e.scale) ? __ldg(e.scale + 2 * w) : (v ? 1.f : 0.f);
+    const float s1 = (v && e.scale) ? __ldg(e.scale + 2 * w + 1) : (v ? 1.f : 0.f);
+    uint64_t r = 0ull;
+    if (t < 9) {
+      if (v) {
+        float lo, hi;
+        f2_unpack(word_to_f2<DT>(__ldg(g + t * cw_real + w)), lo, hi);
+        r = f2_pack(lo * s0, hi * s1);
+      }
+      wsm2[t * cwords + w] = r;
+    } else {
+      if (v && e.bias) r = f2_pack(__ldg(e.bias + 2 * w), __ldg(e.bias + 2 * w + 1));
+      bsm2[w] = r;
+    }
+  }
+}
+
+// K-major operand without swizzle (UMMA "interleave" layout): row m of 16-byte channel chunk q at
+// m * 16 + q * kAlbo. kAlbo = 2064 (not 2048) puts the 8 chunks of one row in distinct bank
+// groups, so a warp's 32 words of one pixel store without bank conflicts. 8-row core matrices are
+// 128 B contiguous (SBO = 128).
+constexpr int kAlbo = 2064;
+constexpr int kAbytes = 17408;  // 8 * kAlbo rounded up to 1 KB (also >= one 128 x 128 B SW128 tile)
+__device__ __forceinline__ uint64_t smem_desc_interleave(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(kAlbo >> 4) << 16;        // LBO: next 16-byte K chunk
+  d |= static_cast<uint64_t>(128 >> 4) << 32;          // SBO: next 8-row group
+  d |= static_cast<uint64_t>(1) << 46;                 // version (sm_100)
+  return d;                                            // layout type 0 = SWIZZLE_NONE
+}
+
+// Ring-buffer position for the single-thread producer / consumer loops: slot index and mbarrier
+// phase advanced incrementally (a runtime `it % n` / `it / n` is a ~25-instruction dependent chain
+// on the critical path of a lone issuing thread).
+struct Ring {
+  int i, n;
+  uint32_t ph;
+  __device__ __forceinline__ explicit Ring(int n_) : i(0), n(n_), ph(0) {}
+  __device__ __forceinline__ void next() {
+    if (++i == n) {
+      i = 0;
+      ph ^= 1u;
+    }
+  }
+};
 
 }  // namespace fcm

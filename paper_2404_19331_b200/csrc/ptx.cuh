@@ -54,13 +54,47 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+#ifndef FCM_MBAR_MODE
+#define FCM_MBAR_MODE 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if FCM_MBAR_MODE == 0
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}"
       ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
+#elif FCM_MBAR_MODE == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+#endif
+}
+
+// Wait for a phase that is usually far away (roles with little work per tile): back off with
+// nanosleep between polls so idle warps do not steal issue slots from the compute warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+               : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  uint32_t ns = 32;
+  while (!done) {
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  }
 }
 
 // ------------------------------------------------------------------ TMA

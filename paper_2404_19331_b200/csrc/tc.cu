@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(576, 1)
     tma_prefetch_desc(&tmb);
     tma_prefetch_desc(&tmy);
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 512); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 16); }
     mbar_init(bfull, 1);
     fence_barrier_init();
   }
@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(576, 1)
                                     if (!(dbg & 16)) tma_store_2d(&tmy, buf, c, m0 + r);
                                   });
       tc_fence_before();
-      mbar_arrive(tempty + acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
       if (threadIdx.x == 0) stamp(local, 5);
     }
     if (lane == 0) bulk_wait_all();
@@ -310,12 +311,18 @@ __global__ void __launch_bounds__(576, 1)
 // the MMA) x one C_out slice of BN channels; the C_in (=K) dimension streams through in
 // 128-byte chunks, so the intermediate "contains all channels" in time, not space.
 // =====================================================================================
-// DW warps per DWPW CTA: 16 for the paired-FP32 bf16/f16 3x3 core (fits 93 registers), else 8.
+// DW warps per DWPW CTA (8: the item counts of 128-pixel tiles divide evenly; more warps idle).
 template <int DT, int K> constexpr int dwpw_ndw() { return 8; }
-constexpr int kDwpwNA = 2;  // A-operand (commBuffer) ring depth
+constexpr int kDwpwNA = 2;  // default A-operand (commBuffer) ring depth
 struct DwDivs {
-  FDiv tw, n16, n8, n4;  // divisors tw and ceil(th / SEG) for SEG = 16, 8, 4
+  FDiv hp, n8, n7, n4;  // column pairs per image, ceil(th / SEG) for SEG = 8, 7, 4
+  FDiv nsplit, tx, ty;  // tile decode
+  int seg_sel;          // SEG per lane-group width: byte g (g = 0, 1, 2 for 32, 16, 8 lanes per slot)
 };
+template <int DT, int K> constexpr bool dwpw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
+template <int DT, int K> constexpr int dwpw_wbytes(int nk) {
+  return dwpw_pair<DT, K>() ? 10 * nk * 32 * 8 : K * K * nk * 32 * 4;
+}
 
 template <int DT, int K, int S>
 __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
                    const __grid_constant__ CUtensorMap tmy, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
                    Epi ep, int N, int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw,
                    int tiles_x, int tiles_y, int nsplit, int BN, int XS, int BS, uint32_t tmem_cols, int ncap, int resB,
-                   DwDivs dv, int dbg) {
+                   DwDivs dv, int na, int nacc, int dbg, unsigned long long* trace) {
   constexpr int V = Tr<DT>::VEC;
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
@@ -338,35 +345,38 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* ostage = smem;                        // 2 x 16 KB output staging
-  uint8_t* abuf = smem + 32768;                  // kDwpwNA x 16 KB A operand (commBuffer) ring
-  uint8_t* xbuf = abuf + kDwpwNA * 16384;        // XS x X halo chunks (TMA -> DW)
+  uint8_t* abuf = smem + 32768;                  // na x kAbytes A operand (commBuffer) ring
+  uint8_t* xbuf = abuf + na * kAbytes;           // XS x X halo chunks (TMA -> DW)
   uint8_t* bbuf = xbuf + XS * xstride;           // BS x PW weight chunks (TMA -> MMA); resB: BS = nk, loaded once
   uint8_t* cst = bbuf + BS * BN * 128;
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(nk * KC));  // DW weights
-  uint8_t* dscr = reinterpret_cast<uint8_t*>(wsm + K * K * nk * 32);  // DW warps' dead-row scratch
+  uint8_t* dscr = reinterpret_cast<uint8_t*>(wsm) + dwpw_wbytes<DT, K>(nk);  // DW warps' dead-row scratch
   uint64_t* fullX = reinterpret_cast<uint64_t*>(dscr + kDwpwNDW * 128);
   uint64_t* emptyX = fullX + XS;
   uint64_t* fullB = emptyX + XS;
   uint64_t* emptyB = fullB + BS;
   uint64_t* afull = emptyB + BS;
-  uint64_t* aempty = afull + kDwpwNA;
-  uint64_t* tfull = aempty + kDwpwNA;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* aempty = afull + na;
+  uint64_t* tfull = aempty + na;
+  uint64_t* tempty = tfull + nacc;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + nacc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cout, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cin, nk * KC, dcst);
-  stage_dw_weights<DT>(wdw, K, Cin, nk * 32, wsm);
-  for (int i = threadIdx.x; i < kDwpwNA * 16384 / 16; i += blockDim.x) sts128(smem_u32(abuf) + 16 * i, 0, 0, 0, 0);
+  constexpr bool kPair = dwpw_pair<DT, K>();
+  uint64_t* wsm2 = reinterpret_cast<uint64_t*>(wsm);  // kPair: scale-folded fp32 pairs [9][nk*32], bias [nk*32]
+  if constexpr (kPair) stage_dw3_f2<DT>(wdw, ed, Cin, nk * 32, wsm2, wsm2 + 9 * nk * 32);
+  else stage_dw_weights<DT>(wdw, K, Cin, nk * 32, wsm);
+  for (int i = threadIdx.x; i < na * kAbytes / 16; i += blockDim.x) sts128(smem_u32(abuf) + 16 * i, 0, 0, 0, 0);
   if (warp == WARP_TX && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
     tma_prefetch_desc(&tmy);
     for (int s = 0; s < XS; ++s) { mbar_init(fullX + s, 1); mbar_init(emptyX + s, kDwpwNDW); }
     for (int s = 0; s < BS; ++s) { mbar_init(fullB + s, 1); mbar_init(emptyB + s, 1); }
-    for (int a = 0; a < kDwpwNA; ++a) { mbar_init(afull + a, kDwpwNDW * 32); mbar_init(aempty + a, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 128); }
+    for (int a = 0; a < na; ++a) { mbar_init(afull + a, kDwpwNDW); mbar_init(aempty + a, 1); }
+    for (int a = 0; a < nacc; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4); }
     fence_barrier_init();
   }
   if (warp == WARP_MMA) tmem_alloc_rt(tslot, tmem_cols);
@@ -376,144 +386,177 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   const uint32_t tbase = *tslot;
   const int spatial = ((N + nb - 1) / nb) * tiles_y * tiles_x;
   const int total = spatial * nsplit;
+  // development tracing (FCM_TRACE): clock64 stamps of CTA 0's first 64 tiles
+#ifdef FCM_TRACE_STAMPS
+  __shared__ unsigned long long tr_sm[64 * 12];  // stamps land in smem (cheap), copied out at exit
+  for (int i = threadIdx.x; i < 64 * 12; i += blockDim.x) tr_sm[i] = 0;
+  __syncthreads();
+#endif
+  auto stamp = [&](int local, int ev) {
+#ifdef FCM_TRACE_STAMPS
+    if (trace && blockIdx.x == 0 && local < 64) tr_sm[local * 12 + ev] = clock64();
+#endif
+  };
+  // tile t -> (C_out split, image group, tile row, tile col) with host-computed magic divisors
   auto decode = [&](int t, int& ns, int& nbi, int& tyi, int& txi) {
-    ns = t % nsplit;
-    int sp = t / nsplit;
-    txi = sp % tiles_x;
-    sp /= tiles_x;
-    tyi = sp % tiles_y;
-    nbi = sp / tiles_y;
+    int sp = fdiv(t, dv.nsplit);
+    ns = t - sp * nsplit;
+    int q = fdiv(sp, dv.tx);
+    txi = sp - q * tiles_x;
+    nbi = fdiv(q, dv.ty);
+    tyi = q - nbi * tiles_y;
   };
 
   if (warp == WARP_TX) {
     if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      Ring rx(XS);
+      int local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         int ns, nbi, tyi, txi;
         decode(t, ns, nbi, tyi, txi);
-        for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % XS;
-          mbar_wait(emptyX + s, ((it / XS) & 1) ^ 1);
-          mbar_arrive_expect_tx(fullX + s, xbytes);
-          tma_load_4d(xbuf + s * xstride, &tmx, fullX + s, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
+        for (int kc = 0; kc < nk; ++kc, rx.next()) {
+          mbar_wait(emptyX + rx.i, rx.ph ^ 1);
+          if (kc == 0) stamp(local, 8);
+          if (kc == nk - 1) stamp(local, 9);
+          mbar_arrive_expect_tx(fullX + rx.i, xbytes);
+          tma_load_4d(xbuf + rx.i * xstride, &tmx, fullX + rx.i, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
         }
       }
     }
   } else if (warp == WARP_TB) {
     if (lane == 0) {
-      int it = 0;
       if (resB) {  // grid is a multiple of nsplit: this CTA's C_out slice is fixed
+        const int ns = blockIdx.x - fdiv(blockIdx.x, dv.nsplit) * nsplit;
         for (int kc = 0; kc < nk; ++kc) {
           mbar_arrive_expect_tx(fullB + kc, BN * 128);
-          tma_load_2d(bbuf + kc * BN * 128, &tmb, fullB + kc, kc * KC, (blockIdx.x % nsplit) * BN);
+          tma_load_2d(bbuf + kc * BN * 128, &tmb, fullB + kc, kc * KC, ns * BN);
         }
       }
+      Ring rb(BS);
       for (int t = blockIdx.x; t < total && !resB; t += gridDim.x) {
-        const int ns = t % nsplit;
-        for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % BS;
-          mbar_wait(emptyB + s, ((it / BS) & 1) ^ 1);
-          mbar_arrive_expect_tx(fullB + s, BN * 128);
-          tma_load_2d(bbuf + s * BN * 128, &tmb, fullB + s, kc * KC, ns * BN);
+        const int ns = t - fdiv(t, dv.nsplit) * nsplit;
+        for (int kc = 0; kc < nk; ++kc, rb.next()) {
+          mbar_wait(emptyB + rb.i, rb.ph ^ 1);
+          mbar_arrive_expect_tx(fullB + rb.i, BN * 128);
+          tma_load_2d(bbuf + rb.i * BN * 128, &tmb, fullB + rb.i, kc * KC, ns * BN);
         }
       }
     }
   } else if (warp == WARP_MMA) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, BN);
-      int it = 0, local = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-        const int acc = local & 1;
-        mbar_wait(tempty + acc, ((local >> 1) & 1) ^ 1);
+      Ring ra(na), rb(BS), rt(nacc);
+      int local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local, rt.next()) {
+        const int acc = rt.i;
+        mbar_wait(tempty + acc, rt.ph ^ 1);
+        stamp(local, 0);
         tc_fence_after();
         const uint32_t d = tbase + acc * BN;
-        for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int a = it % kDwpwNA, sb = resB ? kc : it % BS;
-          mbar_wait(afull + a, (it / kDwpwNA) & 1);
-          mbar_wait(fullB + sb, resB ? 0 : (it / BS) & 1);
+        for (int kc = 0; kc < nk; ++kc, ra.next(), rb.next()) {
+          const int a = ra.i, sb = resB ? kc : rb.i;
+          mbar_wait(afull + a, ra.ph);
+          if (kc == 0) stamp(local, 1);
+          mbar_wait(fullB + sb, resB ? 0 : rb.ph);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(smem_u32(abuf + a * 16384));
+          // kPair: A (the commBuffer) in the no-swizzle K-major layout, a K step = 2 chunks of kAlbo
+          const uint64_t ad = kPair ? smem_desc_interleave(smem_u32(abuf + a * kAbytes))
+                                    : smem_desc_sw128(smem_u32(abuf + a * kAbytes));
+          constexpr uint32_t astep = kPair ? (2 * kAlbo) >> 4 : 2;
           const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + sb * BN * 128));
           const int ksteps = min(4, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
-          for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+          for (int k = 0; k < ksteps && !(dbg & 256); ++k) mma_ss<KIND>(d, ad + astep * k, bd + 2 * k, idesc, (kc | k) != 0);
           mma_commit(aempty + a);
           if (!resB) mma_commit(emptyB + sb);
         }
         mma_commit(tfull + acc);
+        stamp(local, 2);
       }
     }
   } else if (warp >= 4) {
     // ---------------- DW warps: X halo chunk (smem) -> DW -> eps_dw -> A operand (commBuffer)
-    // work item = (output column, segment of kSeg rows), round-robin over the DW warps
-    constexpr bool kPair = (DT == FCM_BF16 || DT == FCM_F16) && K == 3;
-    constexpr int kSeg = kPair ? (S == 1 ? 16 : 8) : 8;
+    constexpr int kSeg = 8;
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
-    const uint32_t lo_c = bound2<DT>(act_lo(ed.act)), hi_c = bound2<DT>(act_hi(ed.act));
-    DwWh<K> W2;
-    uint64_t sc2 = 0, bi2 = 0;
+    const uint32_t hi_c = kPair ? bound2<DT>(act_hi(ed.act)) : 0u;
+    uint64_t W9[9], bias2 = 0ull;
     int kc_w = -1;
-    int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      for (int kc = 0; kc < nk; ++kc, ++it) {
-        const int sx = it % XS, a = it % kDwpwNA;
+    Ring rx(XS), ra(na);
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next()) {
+        const int sx = rx.i, a = ra.i;
         const int c = kc * KC + lane * V;
         const uint32_t st = smem_u32(xbuf + sx * xstride);
-        const uint32_t abase = smem_u32(abuf + a * 16384);
+        const uint32_t abase = smem_u32(abuf + a * kAbytes);
         if constexpr (kPair) {
-          // lane groups: a partially filled chunk (C_in not a multiple of 64) packs 2 or 4 output
-          // columns into one warp (gs = 2^gsl lanes per pixel) instead of idling the empty lanes
+          // lane groups: a partially filled chunk (C_in not a multiple of 64) packs 2 or 4 column
+          // pairs into one warp (slots of 2^gsl lanes) instead of idling the empty lanes
           const int cw_valid = min(32, (Cin - kc * KC) >> 1);
-          const int gsl = cw_valid > 16 ? 5 : (cw_valid > 8 ? 4 : 3);
-          const int npl = 5 - gsl;
+          const int gi = cw_valid > 16 ? 0 : (cw_valid > 8 ? 1 : 2);
+          const int gsl = 5 - gi, npl = gi;
           const int grp = lane >> gsl, wd = lane & ((1 << gsl) - 1);
-          if (kc != kc_w) {  // weights / constants of this chunk (loaded once when nk == 1)
-            const int cl = kc * KC + wd * V;
-            load_dw_weights_h_smem<K>(W2, wsm, nk * 32, kc * 32 + wd);
-            sc2 = f2_pack(dcs.sc(cl), dcs.sc(cl + 1));
-            bi2 = f2_pack(dcs.bi(cl), dcs.bi(cl + 1));
+          if (kc != kc_w) {  // this chunk's scale-folded weights + bias (once per CTA when nk == 1)
+            const uint32_t wa = smem_u32(wsm2) + 8 * (kc * 32 + wd);
+#pragma unroll
+            for (int q = 0; q < 9; ++q) W9[q] = lds64(wa + q * 8 * nk * 32);
+            bias2 = lds64(wa + 9 * 8 * nk * 32);
             kc_w = kc;
           }
-          const bool cval = wd < cw_valid;
-          const int ncg = (nb * tw + (1 << npl) - 1) >> npl;
+          const uint32_t lane_off = (wd >> 2) * kAlbo + (wd & 3) * 4;
           const uint32_t dead = smem_u32(dscr) + (dw * 32 + lane) * 4;
-          mbar_wait(fullX + sx, (it / XS) & 1);
-          mbar_wait(aempty + a, ((it / kDwpwNA) & 1) ^ 1);
-          // segment length adapted to the tile height (compile-time per variant); item -> (column
-          // group, segment) and column -> (image, x) use host-computed magic divisors
-          auto run_items = [&](auto segc, FDiv fnsg) {
+          const int hp = (tw + 1) >> 1;   // column pairs per image row
+          const int ncp = nb * hp;
+          if (dw == 0 && lane == 0 && kc == 0) stamp(local, 10);
+          mbar_wait(fullX + sx, rx.ph);
+          if (dw == 0 && lane == 0 && kc == 0) stamp(local, 6);
+          if (!(dbg & 128)) mbar_wait(aempty + a, ra.ph ^ 1);
+          if (dw == 0 && lane == 0 && kc == 0) stamp(local, 11);
+          // item = (column pair, segment of SEG rows); SEG chosen on the host per lane-group width
+          auto run_items = [&](auto segc, auto actc, FDiv fnsg) {
             constexpr int SEG = decltype(segc)::value;
+            constexpr int ACT = decltype(actc)::value;
             const int nsg = (th + SEG - 1) / SEG;
-            for (int item = dw; item < ncg * nsg && !(dbg & 1); item += kDwpwNDW) {
-              const int cg = fdiv(item, fnsg), seg = item - cg * nsg;
-              const int colr = (cg << npl) + grp;
-              const bool live = colr < nb * tw;
-              const int col = live ? colr : 0;
-              const int b = fdiv(col, dv.tw), x = col - b * tw;
+            const int nit = ncp * nsg;
+            for (int base = dw << npl; base < nit && !(dbg & 1); base += kDwpwNDW << npl) {
+              const int item = base + grp;
+              const bool live = item < nit;
+              const int iv = live ? item : 0;
+              const int cp = fdiv(iv, fnsg), seg = iv - cp * nsg;
+              const int b = fdiv(cp, dv.hp), x0 = 2 * (cp - b * hp);
               const int y0 = seg * SEG;
-              const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + wd) * 4;
-              const int mbase = (b * th + y0) * tw + x;
+              const uint32_t src = st + (((b * th_in) * tw_in + x0 * S) * 32 + wd) * 4;
               const int nvalid = live ? th - y0 : 0;
-              dw_segh<DT, K, S, SEG>(src, 128, tw_in * 128, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
-                // rows past the tile go to a per-lane scratch word: a select, not a branch
-                const uint32_t word = cval ? epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c) : 0u;
-                sts32(r < nvalid ? abase + sw128_off(mbase + r * tw, wd) : dead, word);
-              });
+              const bool c1 = x0 + 1 < tw;
+              const uint32_t a0 = abase + lane_off + (uint32_t)((b * th + y0) * tw + x0) * 16;
+              const uint32_t rstep = (uint32_t)tw * 16;
+              dw3_pair<DT, S, SEG>(src, 128, tw_in * 128, y0, th_in - 1, W9, bias2,
+                                   [&](int r, uint64_t p0, uint64_t p1) {
+                                     const uint32_t ad = a0 + r * rstep;
+                                     const bool rok = r < nvalid;
+                                     sts32(rok ? ad : dead, pack_act<DT, ACT>(p0, hi_c));
+                                     sts32(rok && c1 ? ad + 16 : dead, pack_act<DT, ACT>(p1, hi_c));
+                                   });
             }
           };
-          // longest segment that still gives every DW warp an item (fewer window reloads)
-          if (S == 1 && th > 8 && ncg * ((th + 15) / 16) >= kDwpwNDW) run_items(std::integral_constant<int, 16>(), dv.n16);
-          else if (th > 4 && ncg * ((th + 7) / 8) >= kDwpwNDW / 2) run_items(std::integral_constant<int, 8>(), dv.n8);
-          else run_items(std::integral_constant<int, 4>(), dv.n4);
+          auto run_act = [&](auto segc, FDiv fnsg) {
+            if (ed.act == FCM_ACT_RELU6) run_items(segc, std::integral_constant<int, 2>(), fnsg);
+            else if (ed.act == FCM_ACT_RELU) run_items(segc, std::integral_constant<int, 1>(), fnsg);
+            else run_items(segc, std::integral_constant<int, 0>(), fnsg);
+          };
+          const int seg_sel = (dv.seg_sel >> (8 * gi)) & 0xFF;
+          if (seg_sel == 8) run_act(std::integral_constant<int, 8>(), dv.n8);
+          else if (seg_sel == 7) run_act(std::integral_constant<int, 7>(), dv.n7);
+          else run_act(std::integral_constant<int, 4>(), dv.n4);
         } else {
           DwW<DT, K> W;
           load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + lane);
           EpiC ec[V];
 #pragma unroll
           for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
-          mbar_wait(fullX + sx, (it / XS) & 1);
-          mbar_wait(aempty + a, ((it / kDwpwNA) & 1) ^ 1);
+          mbar_wait(fullX + sx, rx.ph);
+          mbar_wait(aempty + a, ra.ph ^ 1);
           for (int item = dw; item < nitems; item += kDwpwNDW) {
             const int col = item / nseg, seg = item - col * nseg;
             const int b = col / tw, x = col - b * tw;
@@ -527,30 +570,41 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
                                  });
           }
         }
-        fence_proxy_async_smem();
-        mbar_arrive(afull + a);
+        if (!(dbg & 64)) fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(emptyX + sx);
+        if (lane == 0) {
+          mbar_arrive(afull + a);
+          mbar_arrive(emptyX + sx);
+        }
+        if (dw == 0 && lane == 0 && kc == nk - 1) stamp(local, 7);
       }
     }
   } else {
     // ---------------- epilogue warps 0-3: TMEM -> eps_pw -> staging -> TMA store (4-D box)
     int local = 0, sbuf = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const int acc = local & 1;
+    Ring rt(nacc);
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local, rt.next()) {
+      const int acc = rt.i;
       int ns, nbi, tyi, txi;
       decode(t, ns, nbi, tyi, txi);
-      mbar_wait(tfull + acc, (local >> 1) & 1);
+      mbar_wait_sleep(tfull + acc, rt.ph);
+      if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
       if (!(dbg & 2))
         epilogue_tile<DT, 4>(tbase + acc * BN, BN, ns * BN, Cout, cs, ep, ostage, sbuf,
                              [&](const uint8_t* buf, int c) { tma_store_4d(&tmy, buf, c, txi * tw, tyi * th, nbi * nb); });
       tc_fence_before();
-      mbar_arrive(tempty + acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      if (threadIdx.x == 0) stamp(local, 5);
     }
     if (threadIdx.x == 0) bulk_wait_all();
   }
   __syncthreads();
+#ifdef FCM_TRACE_STAMPS
+  if (trace && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < 64 * 12; i += blockDim.x) trace[(i / 12) * 16 + i % 12] = tr_sm[i];
+#endif
   if (warp == WARP_MMA) {
     tc_fence_after();
     tmem_dealloc_rt(tbase, tmem_cols);
@@ -628,9 +682,9 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
     for (int a = 0; a < depth; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, NTP * 32);
-      mbar_init(Tfull + a, NTP * 32);
-      mbar_init(Tempty + a, kPwdwNDW * 32);
+      mbar_init(tempty + a, NTP);  // one arrive per warp (after __syncwarp)
+      mbar_init(Tfull + a, NTP);
+      mbar_init(Tempty + a, kPwdwNDW);
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -755,8 +809,11 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty + acc);
-      mbar_arrive(Tfull + acc);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(tempty + acc);
+        mbar_arrive(Tfull + acc);
+      }
       if (warp == 0 && lane == 0) stamp(local, 5);
     }
   } else {
@@ -828,7 +885,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
                                });
         }
       }
-      mbar_arrive(Tempty + tbi);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(Tempty + tbi);
       if (dw == 0 && lane == 0) stamp(local, 7);
     }
   }
@@ -868,7 +926,7 @@ static void trace_dump(const char* tag) {
   if (!f) return;
   fprintf(f, "# %s\n", tag);
   for (int t = 0; t < 64; ++t) {
-    for (int e = 0; e < 10; ++e) fprintf(f, "%llu ", h[t * 16 + e]);
+    for (int e = 0; e < 12; ++e) fprintf(f, "%llu ", h[t * 16 + e]);
     fprintf(f, "\n");
   }
   fclose(f);
@@ -957,6 +1015,28 @@ int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, 
   return set_error(FCM_E_UNSUPPORTED, "pw tensor-core path: dtype");
 }
 
+// Segment length of the column-pair DW items per lane-group width (1, 2 or 4 slots per warp):
+// the fewest input rows per DW warp (rounds x rows per item, + 2 rows of per-item overhead).
+template <int K, int S>
+static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
+  const int hp = (g.tw + 1) / 2;
+  int sel = 0;
+  for (int gi = 0; gi < 3; ++gi) {
+    const int slots = 1 << gi;
+    int best = 0, bcost = 1 << 30;
+    for (int seg : {8, 7, 4}) {
+      const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
+      const int rounds = ((nit + slots - 1) / slots + ndw - 1) / ndw;
+      const int cost = rounds * ((seg - 1) * S + K + 2);
+      if (cost < bcost) { bcost = cost; best = seg; }
+    }
+    sel |= best << (8 * gi);
+  }
+  const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
+  return DwDivs{make_fdiv(hp),      make_fdiv((g.th + 7) / 8), make_fdiv((g.th + 6) / 7), make_fdiv((g.th + 3) / 4),
+                make_fdiv(nsplit), make_fdiv(tiles_x),        make_fdiv(tiles_y),        sel};
+}
+
 template <int DT, int K, int S>
 static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const void* wp, const Epi& ep, void* y,
                          const Geo& g, int nsplit_req, cudaStream_t st) {
@@ -991,19 +1071,25 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   }
   const int ncap = round_up(nsplit * BN, 16);
   const int nk = (g.C + KC - 1) / KC;
-  const int fixed = 1024 + 32768 + kDwpwNA * 16384 + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + K * K * nk * 128 +
-                    dwpw_ndw<DT, K>() * 128 + 512;
+  static const int na_env = [] { const char* e = getenv("FCM_NA"); return e ? atoi(e) : 0; }();      // dev override
+  static const int nacc_env = [] { const char* e = getenv("FCM_NACC"); return e ? atoi(e) : 0; }();  // dev override
+  const int na = na_env ? na_env : kDwpwNA;
+  int nacc = nacc_env ? nacc_env : 2;
+  while (nacc > 2 && (int)pow2_cols(nacc * BN) > 512) --nacc;
+  const int fixed = 1024 + 32768 + na * kAbytes + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) +
+                    dwpw_wbytes<DT, K>(nk) + dwpw_ndw<DT, K>() * 128 + 512;
   const int xstride = ((g.nb * th_in * tw_in * 128) + 1023) & ~1023;
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
   int grid = std::min(total, device_props().sms);
   int BS = 2;
-  int XS = std::min(6, (device_props().smem_optin - fixed - BS * BN * 128) / xstride);
+  static const int xs_cap = [] { const char* e = getenv("FCM_XS_MAX"); return e ? atoi(e) : 6; }();  // dev override
+  int XS = std::min(xs_cap, (device_props().smem_optin - fixed - BS * BN * 128) / xstride);
   if (XS < 2) return set_error(FCM_E_INFEASIBLE, "dwpw: tile too large for 2 X stages");
   // resident weights: grid a multiple of nsplit fixes each CTA's C_out slice; keep all nk chunks
   // when that costs at most one X stage (and leaves >= 2)
   const int resgrid = (grid / nsplit) * nsplit;
-  const int xs_res = std::min(6, (device_props().smem_optin - fixed - nk * BN * 128) / xstride);
+  const int xs_res = std::min(xs_cap, (device_props().smem_optin - fixed - nk * BN * 128) / xstride);
   const bool resB = nk <= 16 && resgrid > 0 && resgrid >= grid * 15 / 16 && xs_res >= 2 && xs_res >= XS - 1;
   if (resB) {
     grid = resgrid;
@@ -1016,12 +1102,13 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   using TT = typename Tr<DT>::T;
   kern<<<grid, (4 + dwpw_ndw<DT, K>() + 3) * 32, smem, st>>>(tx, tb, ty, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
                                                               g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw,
-                                                              tiles_x, tiles_y, nsplit, BN, XS, BS, pow2_cols(2 * BN),
+                                                              tiles_x, tiles_y, nsplit, BN, XS, BS, pow2_cols(nacc * BN),
                                                               ncap, resB ? 1 : 0,
-                                                              DwDivs{make_fdiv(g.tw), make_fdiv((g.th + 15) / 16),
-                                                                     make_fdiv((g.th + 7) / 8), make_fdiv((g.th + 3) / 4)},
-                                                              debug_flags());
-  return check_launch("dwpw_tc_kernel");
+                                                              dwpw_divs<K, S>(g, dwpw_ndw<DT, K>(), nsplit), na, nacc,
+                                                              debug_flags(), trace_buf());
+  const int rc = check_launch("dwpw_tc_kernel");
+  trace_dump("dwpw");
+  return rc;
 }
 
 template <int DT>

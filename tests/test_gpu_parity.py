@@ -4,6 +4,8 @@ Sizes span several tiles, ragged spatial/channel tails, both strides, k=3/5, eve
 """
 import numpy as np
 import pytest
+
+import synth
 import torch
 
 from tests.cases import Case, as_np, compare, stored
@@ -67,6 +69,23 @@ def test_dwpw(fmt, k, s):
 def test_dwpw_network_shapes_bf16(shape):
     n, h, w, ci, co = shape
     Case("dwpw", "bf16", n, h, w, ci, co, k=3, s=1).check()
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "f16"])
+@pytest.mark.parametrize("act", [synth.ACT_NONE, synth.ACT_RELU, synth.ACT_RELU6])
+def test_dwpw_pair_core_acts_and_partial_chunks(fmt, act):
+    # column-pair FFMA2 DW core: every activation; C_in = 24 (12 words: 16-lane slots) and
+    # 208 = 3 full 64-channel chunks + 16 (8-lane slots); stride 1 and 2
+    Case("dwpw", fmt, 2, 17, 19, 24, 40, k=3, s=1, act_dw=act).check()
+    Case("dwpw", fmt, 2, 17, 19, 208, 24, k=3, s=2, act_dw=act).check()
+
+
+@pytest.mark.parametrize("s", [1, 2])
+def test_dwpw_odd_and_ragged_tiles(s):
+    # odd tile widths leave a single-column last pair; ragged tiles clip at the map edge
+    for tile in [dict(tile_h=7, tile_w=7), dict(tile_h=5, tile_w=9), dict(tile_h=13, tile_w=3),
+                 dict(tile_h=16 // s, tile_w=8), dict(tile_h=4, tile_w=5, tile_n=3)]:
+        Case("dwpw", "bf16", 3, 19, 17, 96, 40, k=3, s=s, tile=tile).check()
 
 
 def test_dwpw_explicit_tiles_and_splits():
