@@ -139,20 +139,20 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tacc, int BN, int n0, int
   }
 }
 
-// Warp-private epilogue (PW): warp w owns TMEM lane quadrant q = w % 4 (32 output rows) and every
-// second 128-byte column chunk (w / 4); it converts its 32 x CPC block into a private SW128
-// staging buffer (two 4 KB buffers, alternating) and its lane 0 issues the TMA store of a
-// (CPC x 32-row) box -- no CTA-wide barriers in the epilogue.
-template <int DT, int G, class StoreFn>
+// Warp-private epilogue (PW): warp w owns TMEM lane quadrant q = w % 4 (32 output rows) and the
+// 128-byte column chunks hs, hs + G, ... ; it converts its 32 x CPC block into a private SW128
+// staging buffer (4 KB) and its lane 0 issues the TMA store of a (CPC x 32-row) box -- no
+// CTA-wide barriers in the epilogue.
+template <int DT, class StoreFn>
 __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0, int N, const EpiS& cs, const Epi& e,
-                                                   uint8_t* wstage, int& sbuf, StoreFn&& store) {
+                                                   uint8_t* wstage, int& sbuf, int hs, int G, StoreFn&& store) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int CPC = 128 / ES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = warp & 3, h = warp >> 2;
+  const int q = warp & 3;
   const int valid = min(BN, N - n0);
   const int nch = (valid + CPC - 1) / CPC;
-  for (int cc = h; cc < nch; cc += G, ++sbuf) {
+  for (int cc = hs; cc < nch; cc += G, ++sbuf) {
     uint8_t* buf = wstage;  // one 4 KB buffer per warp: wait until its previous store has read it
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
@@ -183,13 +183,17 @@ __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0
 }
 
 // =====================================================================================
-// LBL PW: Y[M,N] = eps(X[M,K] . Wp[N,K]^T). Warps 0-7 epilogue, 8 TMA producer, 9 MMA.
+// LBL PW: Y[M,N] = eps(X[M,K] . Wp[N,K]^T). Warps 0-15 epilogue, 16 TMA producer, 17 MMA.
+// The 16 epilogue warps form `ng` groups that take alternate tiles (tile l -> group l % ng), each
+// with its own pair of TMEM accumulators, so the epilogues of ng tiles run concurrently: a tile
+// needs only 4 x nch warps (nch = 128-byte column chunks), and a single group would leave the
+// rest idle while its TMEM round trips serialise.
 // =====================================================================================
 template <int DT>
 __global__ void __launch_bounds__(576, 1)
     pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
-                 const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, int stages,
-                 uint32_t tmem_cols, int ncap, int resB, unsigned long long* trace, int dbg) {
+                 const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, FDiv fnbn,
+                 int stages, int ng, uint32_t tmem_cols, int ncap, int resB, unsigned long long* trace, int dbg) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
@@ -204,17 +208,18 @@ __global__ void __launch_bounds__(576, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(cst + consts_bytes<DT>(ncap));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;
+  uint64_t* tempty = tfull + 8;
+  uint64_t* bfull = tempty + 8;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, N, ncap, cst);
+  const int spg = 4 / ng;  // warps per TMEM lane quadrant in one group
   if (warp == 16 && lane == 0) {
     tma_prefetch_desc(&tma);
     tma_prefetch_desc(&tmb);
     tma_prefetch_desc(&tmy);
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 16); }
+    for (int a = 0; a < 2 * ng; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4 * spg); }
     mbar_init(bfull, 1);
     fence_barrier_init();
   }
@@ -228,69 +233,82 @@ __global__ void __launch_bounds__(576, 1)
   auto stamp = [&](int local, int ev) {
     if (trace && blockIdx.x == 0 && local < 64) trace[local * 16 + ev] = clock64();
   };
+  // tile l of this CTA -> accumulator (group l % ng, alternate buffers) and its phase
+  auto acc_of = [&](int l, int& acc, uint32_t& ph) {
+    const int g = l % ng, j = l / ng;
+    acc = 2 * g + (j & 1);
+    ph = (j >> 1) & 1;
+  };
 
   if (warp == 16) {
     if (lane == 0) {
-      int it = 0, lt = 0;
+      Ring rs(stages);
+      int lt = 0;
       if (resB) {
         // the grid is a multiple of nbn, so this CTA's C_out slice never changes: load it once
         // (a per-tile reload has every SM re-reading the same few KB of L2 each tile)
         mbar_arrive_expect_tx(bfull, nk * BN * 128);
-        for (int kc = 0; kc < nk; ++kc)
-          tma_load_2d(bbuf + kc * BN * 128, &tmb, bfull, kc * KC, (blockIdx.x % nbn) * BN);
+        const int nb0 = blockIdx.x - fdiv(blockIdx.x, fnbn) * nbn;
+        for (int kc = 0; kc < nk; ++kc) tma_load_2d(bbuf + kc * BN * 128, &tmb, bfull, kc * KC, nb0 * BN);
       }
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-        const int m0 = (t / nbn) * 128, n0 = (t % nbn) * BN;
-        for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          mbar_wait(empty + s, ph ^ 1);
+        const int tm = fdiv(t, fnbn);
+        const int m0 = tm * 128, n0 = (t - tm * nbn) * BN;
+        for (int kc = 0; kc < nk; ++kc, rs.next()) {
+          mbar_wait(empty + rs.i, rs.ph ^ 1);
           if (kc == 0) stamp(lt, 8);
-          mbar_arrive_expect_tx(full + s, 16384 + (resB ? 0 : BN * 128));
-          tma_load_2d(abuf + s * 16384, &tma, full + s, kc * KC, m0);
-          if (!resB) tma_load_2d(bbuf + s * BN * 128, &tmb, full + s, kc * KC, n0);
+          mbar_arrive_expect_tx(full + rs.i, 16384 + (resB ? 0 : BN * 128));
+          tma_load_2d(abuf + rs.i * 16384, &tma, full + rs.i, kc * KC, m0);
+          if (!resB) tma_load_2d(bbuf + rs.i * BN * 128, &tmb, full + rs.i, kc * KC, n0);
         }
       }
     }
   } else if (warp == 17) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, BN);
-      int it = 0, local = 0;
+      Ring rs(stages);
+      int local = 0;
       if (resB) mbar_wait(bfull, 0);
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-        const int acc = local & 1;
-        mbar_wait(tempty + acc, ((local >> 1) & 1) ^ 1);
+        int acc;
+        uint32_t ph;
+        acc_of(local, acc, ph);
+        mbar_wait(tempty + acc, ph ^ 1);
         stamp(local, 0);
         tc_fence_after();
         const uint32_t d = tbase + acc * BN;
-        for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % stages;
-          mbar_wait(full + s, (it / stages) & 1);
+        for (int kc = 0; kc < nk; ++kc, rs.next()) {
+          mbar_wait(full + rs.i, rs.ph);
           if (kc == 0) stamp(local, 1);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(smem_u32(abuf + s * 16384));
-          const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + (resB ? kc : s) * BN * 128));
+          const uint64_t ad = smem_desc_sw128(smem_u32(abuf + rs.i * 16384));
+          const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + (resB ? kc : rs.i) * BN * 128));
           const int ksteps = min(4, (K - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
           for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
-          mma_commit(empty + s);
+          mma_commit(empty + rs.i);
         }
         mma_commit(tfull + acc);
         stamp(local, 2);
       }
     }
   } else {
-    int local = 0, sbuf = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const int acc = local & 1;
-      const int m0 = (t / nbn) * 128, n0 = (t % nbn) * BN;
-      mbar_wait(tfull + acc, (local >> 1) & 1);
+    // epilogue warp: lane quadrant q = warp % 4, group g, slot hs within the group
+    const int h = warp >> 2, g = h / spg, hs = h - g * spg;
+    int sbuf = 0;
+    for (int local = g, t = blockIdx.x + g * gridDim.x; t < total; t += ng * gridDim.x, local += ng) {
+      int acc;
+      uint32_t ph;
+      acc_of(local, acc, ph);
+      const int tm = fdiv(t, fnbn);
+      const int m0 = tm * 128, n0 = (t - tm * nbn) * BN;
+      mbar_wait_sleep(tfull + acc, ph);
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
       if (!(dbg & 32))
-        epilogue_tile_warp<DT, 4>(tbase + acc * BN, BN, n0, N, cs, ep, stage + warp * 4096, sbuf,
-                                  [&](const uint8_t* buf, int c, int r) {
-                                    if (!(dbg & 16)) tma_store_2d(&tmy, buf, c, m0 + r);
-                                  });
+        epilogue_tile_warp<DT>(tbase + acc * BN, BN, n0, N, cs, ep, stage + warp * 4096, sbuf, hs, spg,
+                               [&](const uint8_t* buf, int c, int r) {
+                                 if (!(dbg & 16)) tma_store_2d(&tmy, buf, c, m0 + r);
+                               });
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
@@ -779,7 +797,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       uint8_t* tb = tsm + acc * tbytes;
-      mbar_wait(tfull + acc, (local / depth) & 1);
+      mbar_wait_sleep(tfull + acc, (local / depth) & 1);
       if (warp == 0 && lane == 0) stamp(local, 3);
       mbar_wait(Tempty + acc, ((local / depth) & 1) ^ 1);
       if (warp == 0 && lane == 0) stamp(local, 4);
@@ -976,7 +994,7 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   }
   if (!out_tmap_2d(&ty, DT, y, M, N)) return set_error(FCM_E_CUDA, "tensor map (PW Y) failed");
   const int ncap = round_up(nbn * BN, 16);
-  const int fixed = 1024 + 65536 + consts_bytes<DT>(ncap) + 256;
+  const int fixed = 1024 + 65536 + consts_bytes<DT>(ncap) + 512;
   const int budget = device_props().smem_optin - fixed;
   const int nk = (K + KC - 1) / KC;
   const int total = ((M + 127) / 128) * nbn;
@@ -997,10 +1015,16 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
     if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pw: not enough shared memory for 2 stages");
     smem = (size_t)fixed + (size_t)stages * stage_bytes;
   }
+  // epilogue groups: 4 x nch warps per tile, so 4 / nch tiles can drain concurrently (2 TMEM
+  // accumulators per group)
+  const int nchk = (BN * Tr<DT>::ES + 127) / 128;
+  int ng = nchk >= 4 ? 1 : 4 / nchk;
+  if (ng == 3) ng = 2;
+  while (ng > 1 && 2 * ng * BN > 512) ng /= 2;
   auto kern = pw_tc_kernel<DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, 576, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, stages, pow2_cols(2 * BN), ncap, resB ? 1 : 0,
-                                trace_buf(), debug_flags());
+  kern<<<grid, 576, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, make_fdiv(nbn), stages, ng, pow2_cols(2 * ng * BN),
+                                ncap, resB ? 1 : 0, trace_buf(), debug_flags());
   const int rc = check_launch("pw_tc_kernel");
   trace_dump("pw");
   return rc;
