@@ -647,7 +647,13 @@ template <int DT, int K, int S> constexpr int pwdw_seg() {
 }
 struct PwdwDivs {
   FDiv nslice, tx, ty, tw, nseg;  // tile decode + DW item decode
+  FDiv hp, nsg;                   // pair core: column pairs per image, ceil(th / seg)
+  int seg;                        // pair core segment length (4, 7, 8 or 14)
 };
+template <int DT, int K> constexpr bool pwdw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
+template <int DT, int K> constexpr int pwdw_wbytes(int nslice) {
+  return pwdw_pair<DT, K>() ? 10 * nslice * 32 * 8 : K * K * nslice * 128;
+}
 
 template <int DT, int K, int S>
 __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
@@ -682,7 +688,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   uint8_t* cst = bres + (resB ? nk * TD * 128 : 0);
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(ncap));
-  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + K * K * nslice * 32);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(wsm) + pwdw_wbytes<DT, K>(nslice));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 4;
@@ -693,7 +699,9 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cmid, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cmid, ncap, dcst);
-  stage_dw_weights<DT>(wdw, K, Cmid, nslice * 32, wsm);
+  uint64_t* wsm2 = reinterpret_cast<uint64_t*>(wsm);  // pair core: scale-folded fp32 pairs [9][nslice*32] + bias
+  if constexpr (pwdw_pair<DT, K>()) stage_dw3_f2<DT>(wdw, ed, Cmid, nslice * 32, wsm2, wsm2 + 9 * nslice * 32);
+  else stage_dw_weights<DT>(wdw, K, Cmid, nslice * 32, wsm);
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
@@ -841,10 +849,9 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     const int dw = warp - NTP;
     const int nseg = (th + kSeg - 1) / kSeg;
     const int nitems = nb * tw * nseg;
-    const uint32_t lo_c = bound2<DT>(act_lo(ed.act)), hi_c = bound2<DT>(act_hi(ed.act));
+    const uint32_t hi_c = bound2<DT>(act_hi(ed.act));
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
-    DwWh<K> W2;
-    uint64_t sc2 = 0, bi2 = 0;
+    uint64_t W9[9], bias2 = 0ull;
     int sl_w = -1;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -856,30 +863,52 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       const int y0t = tyi * th;
       const int nrows_t = min(th, Ho - y0t);
       if constexpr (kPair) {
-        if (sl != sl_w) {  // this slice's weights / constants (once per CTA with resident slices)
-          load_dw_weights_h_smem<K>(W2, wsm, nslice * 32, sl * 32 + lane);
-          sc2 = f2_pack(dcs.sc(c), dcs.sc(c + 1));
-          bi2 = f2_pack(dcs.bi(c), dcs.bi(c + 1));
+        // column-pair FFMA2 core (as in DWPW): a lane owns one channel word of 2 adjacent output
+        // columns x SEG rows; stores go straight to the NHWC OFM (128 B per warp and pixel)
+        if (sl != sl_w) {  // this slice's weights / bias (once per CTA with resident slices)
+          const uint32_t wa = smem_u32(wsm2) + 8 * (sl * 32 + lane);
+#pragma unroll
+          for (int q = 0; q < 9; ++q) W9[q] = lds64(wa + q * 8 * nslice * 32);
+          bias2 = lds64(wa + 9 * 8 * nslice * 32);
           sl_w = sl;
         }
         const bool cval = c < Cmid;
+        const int hp = (tw + 1) >> 1;
         mbar_wait(Tfull + tbi, (local / depth) & 1);
         if (dw == 0 && lane == 0) stamp(local, 6);
-        for (int item = dw; item < nitems && !(dbg & 1); item += kPwdwNDW) {
-          const int col = fdiv(item, dv.nseg), seg = item - col * nseg;
-          const int b = fdiv(col, dv.tw), x = col - b * tw;
-          const int n = nbi * nb + b, xo = txi * tw + x;
-          const int y0 = seg * kSeg;
-          if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
-          const uint32_t src = tsa + (((b * th_in) * tw_in + x * S) * PW + lane) * 4;
-          const int nvalid = nrows_t - y0;
-          uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
-          const size_t rstride = (size_t)Wo * Cmid / V;
-          dw_segh<DT, K, S, kSeg>(src, PITCH, tw_in * PITCH, y0, th_in - 1, W2, [&](int r, uint64_t acc) {
-            const uint32_t word = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
-            if (r < nvalid && cval) dst[r * rstride] = word;  // predicated store, no branch
-          });
-        }
+        auto run = [&](auto segc, auto actc) {
+          constexpr int SEG = decltype(segc)::value;
+          constexpr int ACT = decltype(actc)::value;
+          const int nsg = (th + SEG - 1) / SEG;
+          const int nit = nb * hp * nsg;
+          for (int item = dw; item < nit && !(dbg & 1); item += kPwdwNDW) {
+            const int cp = fdiv(item, dv.nsg), seg = item - cp * nsg;
+            const int b = fdiv(cp, dv.hp), x0 = 2 * (cp - b * hp);
+            const int n = nbi * nb + b, xo = txi * tw + x0;
+            const int y0 = seg * SEG;
+            if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
+            const uint32_t src = tsa + (((b * th_in) * tw_in + x0 * S) * PW + lane) * 4;
+            const int nvalid = nrows_t - y0;
+            const bool c0ok = cval, c1ok = cval && (x0 + 1 < tw) && (xo + 1 < Wo);
+            uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
+            const size_t rstride = (size_t)Wo * Cmid / V, cstride = (size_t)Cmid / V;
+            dw3_pair<DT, S, SEG>(src, PITCH, tw_in * PITCH, y0, th_in - 1, W9, bias2,
+                                 [&](int r, uint64_t p0, uint64_t p1) {
+                                   const bool rok = r < nvalid;
+                                   if (rok && c0ok) dst[r * rstride] = pack_act<DT, ACT>(p0, hi_c);
+                                   if (rok && c1ok) dst[r * rstride + cstride] = pack_act<DT, ACT>(p1, hi_c);
+                                 });
+          }
+        };
+        auto run_act = [&](auto segc) {
+          if (ed.act == FCM_ACT_RELU6) run(segc, std::integral_constant<int, 2>());
+          else if (ed.act == FCM_ACT_RELU) run(segc, std::integral_constant<int, 1>());
+          else run(segc, std::integral_constant<int, 0>());
+        };
+        if (dv.seg == 14) run_act(std::integral_constant<int, 14>());
+        else if (dv.seg == 8) run_act(std::integral_constant<int, 8>());
+        else if (dv.seg == 7) run_act(std::integral_constant<int, 7>());
+        else run_act(std::integral_constant<int, 4>());
       } else {
         DwW<DT, K> Wd;
         load_dw_weights_smem<DT, K>(Wd, wsm, nslice * 32, sl * 32 + lane);
@@ -1155,6 +1184,23 @@ int launch_dwpw_tc(int dt, const void* x, const void* wdw, const Epi& ed, const 
   return set_error(FCM_E_UNSUPPORTED, "dwpw tensor-core path: dtype");
 }
 
+// PWDW_R tile decode + DW item decode; the pair core's segment length is the one with the fewest
+// input rows per DW warp (rounds x rows per item, + 2 rows of per-item overhead).
+template <int DT, int K, int S>
+static PwdwDivs pwdw_divs(const Geo& g, int nslice, int tiles_x, int tiles_y) {
+  const int hp = (g.tw + 1) / 2;
+  int best = 4, bcost = 1 << 30;
+  for (int seg : {14, 8, 7, 4}) {
+    const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
+    const int rounds = (nit + kPwdwNDW - 1) / kPwdwNDW;
+    const int cost = rounds * ((seg - 1) * S + K + 2);
+    if (cost < bcost) { bcost = cost; best = seg; }
+  }
+  return PwdwDivs{make_fdiv(nslice), make_fdiv(tiles_x), make_fdiv(tiles_y), make_fdiv(g.tw),
+                  make_fdiv((g.th + pwdw_seg<DT, K, S>() - 1) / pwdw_seg<DT, K, S>()), make_fdiv(hp),
+                  make_fdiv((g.th + best - 1) / best), best};
+}
+
 template <int DT, int K, int S>
 static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const void* wdw, const Epi& ed, void* y,
                          const Geo& g, cudaStream_t st) {
@@ -1185,7 +1231,7 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   const int nslice = ncap / TD;
   const int nk = (g.C + KC - 1) / KC;
   const int depth = std::min(3, 512 / (MB * TD));  // TMEM accumulators = T buffers in flight
-  const int fixed = 1024 + 2 * consts_bytes<DT>(ncap) + K * K * nslice * 128 + 512;
+  const int fixed = 1024 + 2 * consts_bytes<DT>(ncap) + pwdw_wbytes<DT, K>(nslice) + 512;
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nslice;
   int grid = std::min(total, device_props().sms);
@@ -1218,10 +1264,7 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
                                                      static_cast<uint8_t*>(y), g.N, g.H, g.W, g.C, g.Ho, g.Wo, g.Cout,
                                                      g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages, dep,
                                                      pow2_cols(dep * MB * TD), ncap, resB ? 1 : 0,
-                                                     PwdwDivs{make_fdiv(nslice), make_fdiv(tiles_x), make_fdiv(tiles_y),
-                                                              make_fdiv(g.tw),
-                                                              make_fdiv((g.th + pwdw_seg<DT, K, S>() - 1) /
-                                                                        pwdw_seg<DT, K, S>())},
+                                                     pwdw_divs<DT, K, S>(g, nslice, tiles_x, tiles_y),
                                                      debug_flags(), trace_buf());
   const int rc = check_launch("pwdw_tc_kernel");
   trace_dump("pwdw");
