@@ -247,7 +247,7 @@ int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, con
   if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y))
     return launch_dwpw_simt(x->dtype, x->data, w_dw, to_epi(ep_dw), w_pw_packed, to_epi(ep_pw), y->data, g, st);
   int nsplit = 0;
-  default_dwpw_tile(g);
+  default_dwpw_tile(g, dwpw_mmax(x->dtype, g), dwpw_pair_dt(x->dtype, g));
   if (tile) {
     if (tile->tile_h > 0) g.th = tile->tile_h;
     if (tile->tile_w > 0) g.tw = tile->tile_w;

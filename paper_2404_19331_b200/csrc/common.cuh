@@ -588,6 +588,14 @@ __device__ __forceinline__ void stage_dw3_f2(const void* wdw, const Epi& e, int 
 // 128 B contiguous (SBO = 128).
 constexpr int kAlbo = 2064;
 constexpr int kAbytes = 17408;  // 8 * kAlbo rounded up to 1 KB (also >= one 128 x 128 B SW128 tile)
+__device__ __forceinline__ uint64_t smem_desc_interleave(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;  // LBO: next 16-byte K chunk
+  d |= static_cast<uint64_t>(128 >> 4) << 32;            // SBO: next 8-row group
+  d |= static_cast<uint64_t>(1) << 46;                   // version (sm_100)
+  return d;                                              // layout type 0 = SWIZZLE_NONE
+}
 __device__ __forceinline__ uint64_t smem_desc_interleave(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);

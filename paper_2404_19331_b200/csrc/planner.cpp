@@ -290,10 +290,11 @@ static Cost b200_dwpw(const Layer& d, const Layer& p, ll N, int dt, ll b, const 
   if (dt == FCM_F32 || !aligned16(d.C, b) || !aligned16(Co, b)) {
     g.nb = 1; g.th = 8; g.tw = 8; bn = 64;
   } else {
-    default_dwpw_tile(g);
+    const int mmax = dwpw_mmax(dt, g);
+    default_dwpw_tile(g, mmax, dwpw_pair_dt(dt, g));
     int nb_out = 0;
     bn = pick_bn((int)Co, 0, (int)(128 / b), nb_out);
-    if (!dwpw_tile_ok(g, g.nb, g.th, g.tw)) return c;
+    if (!dwpw_tile_ok(g, g.nb, g.th, g.tw, mmax)) return c;
   }
   c.ok = true;
   c.nb = g.nb; c.th = g.th; c.tw = g.tw; c.nsplit = cdiv(Co, bn);

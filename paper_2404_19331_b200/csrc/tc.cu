@@ -325,9 +325,11 @@ __global__ void __launch_bounds__(576, 1)
 
 // =====================================================================================
 // FCM DWPW. Warps 0-3 PW epilogue, 4..4+NDW-1 DW producers of the A operand (commBuffer),
-// then one TMA warp and one MMA warp. One tile = nb x th x tw output pixels (<= 128 rows of
-// the MMA) x one C_out slice of BN channels; the C_in (=K) dimension streams through in
-// 128-byte chunks, so the intermediate "contains all channels" in time, not space.
+// then one TMA warp and one MMA warp. One tile = nb x th x tw output pixels (MB <= 2 MMA row
+// blocks of 128: M <= 256 for the bf16/f16 3x3 pair core, else <= 128) x one C_out slice of BN
+// channels; the C_in (=K) dimension streams through in 128-byte chunks, so the intermediate
+// "contains all channels" in time, not space. The PW epilogue stores straight from
+// registers (a lane owns one output pixel: its BN channels are contiguous in NHWC).
 // =====================================================================================
 // DW warps per DWPW CTA (8: the item counts of 128-pixel tiles divide evenly; more warps idle).
 template <int DT, int K> constexpr int dwpw_ndw() { return 8; }
@@ -335,6 +337,7 @@ constexpr int kDwpwNA = 2;  // default A-operand (commBuffer) ring depth
 struct DwDivs {
   FDiv hp, n8, n7, n4;  // column pairs per image, ceil(th / SEG) for SEG = 8, 7, 4
   FDiv nsplit, tx, ty;  // tile decode
+  FDiv thw, tw;         // epilogue: MMA row m -> (image, row, col) of the tile
   int seg_sel;          // SEG per lane-group width: byte g (g = 0, 1, 2 for 32, 16, 8 lanes per slot)
 };
 template <int DT, int K> constexpr bool dwpw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
@@ -345,10 +348,10 @@ template <int DT, int K> constexpr int dwpw_wbytes(int nk) {
 template <int DT, int K, int S>
 __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
     dwpw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
-                   const __grid_constant__ CUtensorMap tmy, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
+                   void* __restrict__ tmy_base, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
                    Epi ep, int N, int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw,
                    int tiles_x, int tiles_y, int nsplit, int BN, int XS, int BS, uint32_t tmem_cols, int ncap, int resB,
-                   DwDivs dv, int na, int nacc, int dbg, unsigned long long* trace) {
+                   DwDivs dv, int na, int nacc, int MB, int albo, int dbg, unsigned long long* trace) {
   constexpr int V = Tr<DT>::VEC;
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
@@ -362,9 +365,11 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   const int nk = (Cin + KC - 1) / KC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* ostage = smem;                        // 2 x 16 KB output staging
-  uint8_t* abuf = smem + 32768;                  // na x kAbytes A operand (commBuffer) ring
-  uint8_t* xbuf = abuf + na * kAbytes;           // XS x X halo chunks (TMA -> DW)
+  constexpr bool kPair = dwpw_pair<DT, K>();
+  // A slot: pair core = no-swizzle K-major rows (MB x 128 rows, LBO = albo); else SW128, 128 rows
+  const int aslot = kPair ? ((8 * albo + 1023) & ~1023) : 16384;
+  uint8_t* abuf = smem;                          // na x aslot A operand (commBuffer) ring
+  uint8_t* xbuf = abuf + na * aslot;             // XS x X halo chunks (TMA -> DW)
   uint8_t* bbuf = xbuf + XS * xstride;           // BS x PW weight chunks (TMA -> MMA); resB: BS = nk, loaded once
   uint8_t* cst = bbuf + BS * BN * 128;
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
@@ -382,15 +387,13 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cout, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cin, nk * KC, dcst);
-  constexpr bool kPair = dwpw_pair<DT, K>();
   uint64_t* wsm2 = reinterpret_cast<uint64_t*>(wsm);  // kPair: scale-folded fp32 pairs [9][nk*32], bias [nk*32]
   if constexpr (kPair) stage_dw3_f2<DT>(wdw, ed, Cin, nk * 32, wsm2, wsm2 + 9 * nk * 32);
   else stage_dw_weights<DT>(wdw, K, Cin, nk * 32, wsm);
-  for (int i = threadIdx.x; i < na * kAbytes / 16; i += blockDim.x) sts128(smem_u32(abuf) + 16 * i, 0, 0, 0, 0);
+  for (int i = threadIdx.x; i < na * aslot / 16; i += blockDim.x) sts128(smem_u32(abuf) + 16 * i, 0, 0, 0, 0);
   if (warp == WARP_TX && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmb);
-    tma_prefetch_desc(&tmy);
     for (int s = 0; s < XS; ++s) { mbar_init(fullX + s, 1); mbar_init(emptyX + s, kDwpwNDW); }
     for (int s = 0; s < BS; ++s) { mbar_init(fullB + s, 1); mbar_init(emptyB + s, 1); }
     for (int a = 0; a < na; ++a) { mbar_init(afull + a, kDwpwNDW); mbar_init(aempty + a, 1); }
@@ -470,20 +473,23 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
         mbar_wait(tempty + acc, rt.ph ^ 1);
         stamp(local, 0);
         tc_fence_after();
-        const uint32_t d = tbase + acc * BN;
+        const uint32_t d = tbase + acc * (MB * BN);
         for (int kc = 0; kc < nk; ++kc, ra.next(), rb.next()) {
           const int a = ra.i, sb = resB ? kc : rb.i;
           mbar_wait(afull + a, ra.ph);
           if (kc == 0) stamp(local, 1);
           mbar_wait(fullB + sb, resB ? 0 : rb.ph);
           tc_fence_after();
-          // kPair: A (the commBuffer) in the no-swizzle K-major layout, a K step = 2 chunks of kAlbo
-          const uint64_t ad = kPair ? smem_desc_interleave(smem_u32(abuf + a * kAbytes))
-                                    : smem_desc_sw128(smem_u32(abuf + a * kAbytes));
-          constexpr uint32_t astep = kPair ? (2 * kAlbo) >> 4 : 2;
+          // kPair: A (the commBuffer) in the no-swizzle K-major layout, a K step = 2 chunks of albo,
+          // row block h starts 128 rows (2 KB) further
+          const uint64_t ad = kPair ? smem_desc_interleave(smem_u32(abuf + a * aslot), albo)
+                                    : smem_desc_sw128(smem_u32(abuf + a * aslot));
+          const uint32_t astep = kPair ? (2 * albo) >> 4 : 2;
           const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + sb * BN * 128));
           const int ksteps = min(4, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
-          for (int k = 0; k < ksteps && !(dbg & 256); ++k) mma_ss<KIND>(d, ad + astep * k, bd + 2 * k, idesc, (kc | k) != 0);
+          for (int h = 0; h < MB; ++h)
+            for (int k = 0; k < ksteps && !(dbg & 256); ++k)
+              mma_ss<KIND>(d + h * BN, ad + h * (2048 >> 4) + astep * k, bd + 2 * k, idesc, (kc | k) != 0);
           mma_commit(aempty + a);
           if (!resB) mma_commit(emptyB + sb);
         }
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
         const int sx = rx.i, a = ra.i;
         const int c = kc * KC + lane * V;
         const uint32_t st = smem_u32(xbuf + sx * xstride);
-        const uint32_t abase = smem_u32(abuf + a * kAbytes);
+        const uint32_t abase = smem_u32(abuf + a * aslot);
         if constexpr (kPair) {
           // lane groups: a partially filled chunk (C_in not a multiple of 64) packs 2 or 4 column
           // pairs into one warp (slots of 2^gsl lanes) instead of idling the empty lanes
@@ -522,7 +528,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
             bias2 = lds64(wa + 9 * 8 * nk * 32);
             kc_w = kc;
           }
-          const uint32_t lane_off = (wd >> 2) * kAlbo + (wd & 3) * 4;
+          const uint32_t lane_off = (wd >> 2) * albo + (wd & 3) * 4;
           const uint32_t dead = smem_u32(dscr) + (dw * 32 + lane) * 4;
           const int hp = (tw + 1) >> 1;   // column pairs per image row
           const int ncp = nb * hp;
@@ -598,25 +604,56 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps 0-3: TMEM -> eps_pw -> staging -> TMA store (4-D box)
-    int local = 0, sbuf = 0;
+    // ---------------- epilogue warps 0-3: TMEM -> eps_pw -> global (lane = one output pixel)
+    int local = 0;
     Ring rt(nacc);
+    const int q = warp & 3;
+    const int tpx = nb * th * tw;
+    uint8_t* yb = static_cast<uint8_t*>(tmy_base);
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local, rt.next()) {
       const int acc = rt.i;
       int ns, nbi, tyi, txi;
       decode(t, ns, nbi, tyi, txi);
+      const int valid = min(BN, Cout - ns * BN);
       mbar_wait_sleep(tfull + acc, rt.ph);
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
-      if (!(dbg & 2))
-        epilogue_tile<DT, 4>(tbase + acc * BN, BN, ns * BN, Cout, cs, ep, ostage, sbuf,
-                             [&](const uint8_t* buf, int c) { tma_store_4d(&tmy, buf, c, txi * tw, tyi * th, nbi * nb); });
+      for (int h = 0; h < MB && !(dbg & 2); ++h) {
+        const int m = h * 128 + q * 32 + lane;
+        const int b = fdiv(m, dv.thw), rem = m - b * (th * tw);
+        const int yy = fdiv(rem, dv.tw), xx = rem - yy * tw;
+        const int n = nbi * nb + b, yo = tyi * th + yy, xo = txi * tw + xx;
+        const bool ok = m < tpx && n < N && yo < Ho && xo < Wo;
+        uint8_t* dst = yb + ((((size_t)n * Ho + yo) * Wo + xo) * Cout + (size_t)ns * BN) * ES;
+        const uint32_t tq = tbase + acc * (MB * BN) + h * BN + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+        for (int c0 = 0; c0 < valid; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tq + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int cb = c0 + 16 * hh;  // 16 columns = 2 x 8-column (16 B bf16 / 8 B int8) pieces
+            if (cb >= valid) break;
+            uint32_t o[8];
+            epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o);
+            if (ok) {
+              if constexpr (ES == 2) {
+                stg128(dst + cb * 2, o[0], o[1], o[2], o[3]);
+                if (cb + 8 < valid) stg128(dst + cb * 2 + 16, o[4], o[5], o[6], o[7]);
+              } else {
+                if (cb + 8 < valid) stg128(dst + cb, o[0], o[1], o[2], o[3]);
+                else stg64(dst + cb, o[0], o[1]);
+              }
+            }
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
       if (threadIdx.x == 0) stamp(local, 5);
     }
-    if (threadIdx.x == 0) bulk_wait_all();
   }
   __syncthreads();
 #ifdef FCM_TRACE_STAMPS
@@ -1087,7 +1124,8 @@ static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
   }
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   return DwDivs{make_fdiv(hp),      make_fdiv((g.th + 7) / 8), make_fdiv((g.th + 6) / 7), make_fdiv((g.th + 3) / 4),
-                make_fdiv(nsplit), make_fdiv(tiles_x),        make_fdiv(tiles_y),        sel};
+                make_fdiv(nsplit), make_fdiv(tiles_x),        make_fdiv(tiles_y),        make_fdiv(g.th * g.tw),
+                make_fdiv(g.tw),   sel};
 }
 
 template <int DT, int K, int S>
@@ -1095,12 +1133,18 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
                          const Geo& g, int nsplit_req, cudaStream_t st) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
+  constexpr bool kPair = dwpw_pair<DT, K>();
   const int th_in = (g.th - 1) * S + K, tw_in = (g.tw - 1) * S + K;
-  if (g.nb * g.th * g.tw > 128) return set_error(FCM_E_INFEASIBLE, "dwpw: tile has more than 128 pixels");
+  const int tpx = g.nb * g.th * g.tw;
+  if (tpx > (kPair ? 256 : 128))
+    return set_error(FCM_E_INFEASIBLE, "dwpw: tile has more pixels than the MMA rows (256 pair core, else 128)");
   if (th_in > 256 || tw_in > 256 || g.nb > 256) return set_error(FCM_E_INFEASIBLE, "dwpw: halo box > 256");
+  const int MB = (tpx + 127) / 128;            // MMA row blocks of 128
+  const int albo = 16 * 128 * MB + 16;          // interleave LBO (padded: conflict-free DW stores)
   int nsplit = 0;
   const int BN = pick_bn<DT>(g.Cout, nsplit_req, nsplit);
-  CUtensorMap tx, tb, ty;
+  if (2 * MB * BN > 512) return set_error(FCM_E_INFEASIBLE, "dwpw: 2 x (tile rows / 128) x C_out slice > 512 TMEM columns");
+  CUtensorMap tx, tb;
   {
     const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
     const uint64_t str[3] = {(uint64_t)g.C * ES, (uint64_t)g.W * g.C * ES, (uint64_t)g.H * g.W * g.C * ES};
@@ -1115,22 +1159,14 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
     if (!encode_tmap(&tb, tmap_dtype(DT), 2, wp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return set_error(FCM_E_CUDA, "tensor map (DWPW B) failed");
   }
-  {
-    const uint64_t dims[4] = {(uint64_t)g.Cout, (uint64_t)g.Wo, (uint64_t)g.Ho, (uint64_t)g.N};
-    const uint64_t str[3] = {(uint64_t)g.Cout * ES, (uint64_t)g.Wo * g.Cout * ES, (uint64_t)g.Ho * g.Wo * g.Cout * ES};
-    const uint32_t box[4] = {(uint32_t)(128 / ES), (uint32_t)g.tw, (uint32_t)g.th, (uint32_t)g.nb};
-    if (!encode_tmap(&ty, tmap_dtype(DT), 4, y, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
-      return set_error(FCM_E_CUDA, "tensor map (DWPW Y) failed");
-  }
   const int ncap = round_up(nsplit * BN, 16);
   const int nk = (g.C + KC - 1) / KC;
-  static const int na_env = [] { const char* e = getenv("FCM_NA"); return e ? atoi(e) : 0; }();      // dev override
-  static const int nacc_env = [] { const char* e = getenv("FCM_NACC"); return e ? atoi(e) : 0; }();  // dev override
+  static const int na_env = [] { const char* e = getenv("FCM_NA"); return e ? atoi(e) : 0; }();  // dev override
   const int na = na_env ? na_env : kDwpwNA;
-  int nacc = nacc_env ? nacc_env : 2;
-  while (nacc > 2 && (int)pow2_cols(nacc * BN) > 512) --nacc;
-  const int fixed = 1024 + 32768 + na * kAbytes + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) +
-                    dwpw_wbytes<DT, K>(nk) + dwpw_ndw<DT, K>() * 128 + 512;
+  const int nacc = 2;
+  const int aslot = kPair ? ((8 * albo + 1023) & ~1023) : 16384;
+  const int fixed = 1024 + na * aslot + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + dwpw_wbytes<DT, K>(nk) +
+                    dwpw_ndw<DT, K>() * 128 + 512;
   const int xstride = ((g.nb * th_in * tw_in * 128) + 1023) & ~1023;
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
@@ -1153,12 +1189,12 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   auto kern = dwpw_tc_kernel<DT, K, S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   using TT = typename Tr<DT>::T;
-  kern<<<grid, (4 + dwpw_ndw<DT, K>() + 3) * 32, smem, st>>>(tx, tb, ty, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
+  DwDivs dv = dwpw_divs<K, S>(g, dwpw_ndw<DT, K>(), nsplit);
+  kern<<<grid, (4 + dwpw_ndw<DT, K>() + 3) * 32, smem, st>>>(tx, tb, y, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
                                                               g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw,
-                                                              tiles_x, tiles_y, nsplit, BN, XS, BS, pow2_cols(nacc * BN),
-                                                              ncap, resB ? 1 : 0,
-                                                              dwpw_divs<K, S>(g, dwpw_ndw<DT, K>(), nsplit), na, nacc,
-                                                              debug_flags(), trace_buf());
+                                                              tiles_x, tiles_y, nsplit, BN, XS, BS,
+                                                              pow2_cols(nacc * MB * BN), ncap, resB ? 1 : 0, dv, na,
+                                                              nacc, MB, albo, debug_flags(), trace_buf());
   const int rc = check_launch("dwpw_tc_kernel");
   trace_dump("dwpw");
   return rc;

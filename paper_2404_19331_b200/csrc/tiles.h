@@ -28,32 +28,58 @@ inline void default_dw_tile(Geo& g) {
 }
 
 // Cost of one DWPW tiling: DW rows computed (incl. ragged edges) + half the staged halo + a
-// fixed per-tile overhead, all x number of tiles. Candidates respect M <= 128, box <= 256 and a
-// 2-stage smem budget.
+// fixed per-tile (per C_in-chunk phase) overhead, all x number of tiles. The overhead constant
+// (96 pixel-equivalents) reflects the measured hand-off cost of a phase on B200 (~800 cycles vs
+// ~1000 cycles of DW work per 128 pixels x 64 channels).
 inline long dwpw_tile_cost(const Geo& g, int nb, int th, int tw) {
   const int th_in = halo(th, g.k, g.s), tw_in = halo(tw, g.k, g.s);
   const long tiles = (long)((g.N + nb - 1) / nb) * ((g.Ho + th - 1) / th) * ((g.Wo + tw - 1) / tw);
-  return tiles * (2L * nb * th * tw + (long)nb * th_in * tw_in + 32);
+  return tiles * (2L * nb * th * tw + (long)nb * th_in * tw_in + 96);
 }
 
-inline bool dwpw_tile_ok(const Geo& g, int nb, int th, int tw) {
+// Largest DWPW tile (MMA rows): 256 (two M=128 blocks) for the bf16/f16 3x3 pair core when
+// 2 x 2 x C_out fits the 512 TMEM columns, else 128.
+inline bool dwpw_pair_dt(int dt, const Geo& g) { return (dt == FCM_BF16 || dt == FCM_F16) && g.k == 3; }
+inline int dwpw_mmax(int dt, const Geo& g) { return (dwpw_pair_dt(dt, g) && g.Cout <= 128) ? 256 : 128; }
+
+inline bool dwpw_tile_ok(const Geo& g, int nb, int th, int tw, int mmax = 128) {
   const int th_in = halo(th, g.k, g.s), tw_in = halo(tw, g.k, g.s);
-  if (nb * th * tw > 128 || th_in > 256 || tw_in > 256) return false;
-  // mirror of launch_dwpw_t's layout: staging 32K + A ring 2x16K + B ring 2x(BN<=256)x128
-  // + constants / DW weights (<= 24K) + at least 2 X stages
+  if (nb * th * tw > mmax || th_in > 256 || tw_in > 256) return false;
+  // mirror of launch_dwpw_t's layout: A ring 2 x (8 chunks x (rows x 16 B + 16)) + B ring
+  // 2 x BN x 128 + constants / DW weights (<= 40K) + at least 2 X stages
+  const int mb = (nb * th * tw + 127) / 128;
+  const int aslot = ((8 * (16 * 128 * mb + 16)) + 1023) & ~1023;
+  const int bn = std::min(256, (g.Cout + 15) / 16 * 16);
   const int xstride = ((nb * th_in * tw_in * 128) + 1023) & ~1023;
-  return 1024 + 32768 + 2 * 16384 + 2 * 256 * 128 + 24576 + 1536 + 2 * xstride <= 232448;
+  return 1024 + 2 * aslot + 2 * bn * 128 + 40960 + 1536 + 2 * xstride <= 232448;
 }
 
-inline void default_dwpw_tile(Geo& g) {
+// Pair-core (bf16/f16 3x3) DWPW tile time in "DW row" units: a C_in-chunk phase costs the
+// slowest DW warp's rows (rounds x (SEG + 2) over 8 warps, best SEG of 8/7/4) plus ~10 rows of
+// hand-off; tiles run in waves of #SMs.
+inline long dwpw_pair_cost(const Geo& g, int nb, int th, int tw, int sms = 148) {
+  const long tiles = (long)((g.N + nb - 1) / nb) * ((g.Ho + th - 1) / th) * ((g.Wo + tw - 1) / tw);
+  const int hp = (tw + 1) / 2;
+  long best = -1;
+  for (int seg : {8, 7, 4}) {
+    const int items = nb * hp * ((th + seg - 1) / seg);
+    const long t = (long)((items + 7) / 8) * ((seg - 1) * g.s + 3 + 2);
+    if (best < 0 || t < best) best = t;
+  }
+  const int halo_px = nb * halo(th, g.k, g.s) * halo(tw, g.k, g.s);  // TMA / smem fill of the halo tile
+  return ((tiles + sms - 1) / sms) * (best + 10 + halo_px / 64);
+}
+
+inline void default_dwpw_tile(Geo& g, int mmax = 128, bool pair = false) {
   long best = -1;
   int bn = 1, bh = 1, bw = 1;
   for (int tw = 1; tw <= std::min(g.Wo, 64); ++tw)
-    for (int th = 1; th <= std::min(g.Ho, 128 / tw); ++th) {
-      const int nbmax = (th == g.Ho && tw == g.Wo) ? std::max(1, std::min(g.N, 128 / (th * tw))) : 1;
+    for (int th = 1; th <= std::min(g.Ho, mmax / tw); ++th) {
+      const int nbmax = (th == g.Ho && tw == g.Wo) ? std::max(1, std::min(g.N, mmax / (th * tw))) : 1;
       for (int nb = 1; nb <= nbmax; ++nb) {
-        if (!dwpw_tile_ok(g, nb, th, tw)) continue;
-        const long c = dwpw_tile_cost(g, nb, th, tw);
+        if (!dwpw_tile_ok(g, nb, th, tw, mmax)) continue;
+        if (pair && tw < std::min(4, g.Wo)) continue;  // thin columns: halo re-reads dominate
+        const long c = pair ? dwpw_pair_cost(g, nb, th, tw) : dwpw_tile_cost(g, nb, th, tw);
         if (best < 0 || c < best) { best = c; bn = nb; bh = th; bw = tw; }
       }
     }

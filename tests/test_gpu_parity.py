@@ -88,6 +88,15 @@ def test_dwpw_odd_and_ragged_tiles(s):
         Case("dwpw", "bf16", 3, 19, 17, 96, 40, k=3, s=s, tile=tile).check()
 
 
+def test_dwpw_two_row_block_tiles():
+    # pair-core tiles of 129..256 pixels: two M=128 MMA row blocks, direct register epilogue
+    # (stride 2 halos of such tiles do not fit two smem stages; the tile chooser never picks them)
+    for tile in [dict(tile_h=16, tile_w=16), dict(tile_h=14, tile_w=14), dict(tile_h=28, tile_w=7),
+                 dict(tile_h=7, tile_w=7, tile_n=5), dict(tile_h=13, tile_w=11)]:
+        Case("dwpw", "bf16", 5, 30, 29, 96, 40, k=3, s=1, tile=tile).check()
+    Case("dwpw", "f16", 2, 33, 35, 24, 16, k=3, s=1, tile=dict(tile_h=16, tile_w=16)).check()
+
+
 def test_dwpw_explicit_tiles_and_splits():
     for tile in [dict(tile_h=4, tile_w=8), dict(tile_h=8, tile_w=16, n_split=2), dict(tile_h=7, tile_w=7, tile_n=2)]:
         Case("dwpw", "bf16", 3, 14, 14, 64, 96, tile=tile).check()
