@@ -5,11 +5,13 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "common.cuh"
+
 #include "host.h"
 #include "tiles.h"
 
@@ -51,6 +53,11 @@ const DevProps& device_props() {
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool pdl_enabled() {
+  static const bool on = [] { const char* e = getenv("FCM_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
 
 bool encode_tmap(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* base, const uint64_t* dims,
                  const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {

@@ -17,6 +17,8 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
                                                       const typename Tr<DT>::T* __restrict__ wdw, Epi ep,
                                                       typename Tr<DT>::T* __restrict__ y, int C, int Ho, int Wo,
                                                       int pt, int pl, int th, int tw, int tiles_x, int tiles_y) {
+  pdl_launch();
+  pdl_wait();
   constexpr int V = Tr<DT>::VEC;
   constexpr int KC = 32 * V;  // channels per 128-byte group
   extern __shared__ __align__(128) uint32_t xs[];
@@ -104,6 +106,8 @@ template <int DT>
 __global__ void dw_nchw_kernel(const typename Tr<DT>::T* __restrict__ x, const typename Tr<DT>::T* __restrict__ wdw,
                                Epi ep, typename Tr<DT>::T* __restrict__ y, int C, int H, int W, int Ho, int Wo, int k,
                                int s, int pt, int pl, long long total) {
+  pdl_launch();
+  pdl_wait();
   using TT = typename Tr<DT>::T;
   using A = typename Tr<DT>::acc_t;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -140,6 +144,8 @@ __global__ void dw_nchw_kernel(const typename Tr<DT>::T* __restrict__ x, const t
 // Offline PW packing: canonical [C_in][C_out] -> K-major [C_out][C_in].
 template <typename TT>
 __global__ void pack_pw_kernel(const TT* __restrict__ w, TT* __restrict__ p, int cin, int cout) {
+  pdl_launch();
+  pdl_wait();
   __shared__ TT tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx over cout, by over cin
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -174,7 +180,7 @@ static int launch_dw_t(const void* x, const void* wdw, const Epi& ep, void* y, c
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(tiles_x * tiles_y * g.N, (g.C + KC - 1) / KC);
   using TT = typename Tr<DT>::T;
-  kern<<<grid, 128, smem, st>>>(tm, static_cast<const TT*>(wdw), ep, static_cast<TT*>(y), g.C, g.Ho, g.Wo, g.pt, g.pl,
+  launch_k(kern, dim3(grid), dim3(128), smem, st, tm, static_cast<const TT*>(wdw), ep, static_cast<TT*>(y), g.C, g.Ho, g.Wo, g.pt, g.pl,
                                 th, tw, tiles_x, tiles_y);
   return check_launch("dw_nhwc_kernel");
 }
@@ -203,7 +209,7 @@ static int launch_dw_nchw_t(const void* x, const void* wdw, const Epi& ep, void*
   using TT = typename Tr<DT>::T;
   const long long total = (long long)g.N * g.C * g.Ho * g.Wo;
   const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)device_props().sms * 16);
-  dw_nchw_kernel<DT><<<blocks, 256, 0, st>>>(static_cast<const TT*>(x), static_cast<const TT*>(wdw), ep,
+  launch_k(dw_nchw_kernel<DT>, dim3(blocks), dim3(256), 0, st, static_cast<const TT*>(x), static_cast<const TT*>(wdw), ep,
                                              static_cast<TT*>(y), g.C, g.H, g.W, g.Ho, g.Wo, g.k, g.s, g.pt, g.pl,
                                              total);
   return check_launch("dw_nchw_kernel");
@@ -222,9 +228,9 @@ int launch_dw_nchw(int dt, const void* x, const void* wdw, const Epi& ep, void* 
 int launch_pack_pw(int dt, int cin, int cout, const void* w, void* packed, cudaStream_t st) {
   dim3 grid((cout + 31) / 32, (cin + 31) / 32), block(32, 8);
   switch (elem_size(dt)) {
-    case 4: pack_pw_kernel<uint32_t><<<grid, block, 0, st>>>((const uint32_t*)w, (uint32_t*)packed, cin, cout); break;
-    case 2: pack_pw_kernel<uint16_t><<<grid, block, 0, st>>>((const uint16_t*)w, (uint16_t*)packed, cin, cout); break;
-    default: pack_pw_kernel<uint8_t><<<grid, block, 0, st>>>((const uint8_t*)w, (uint8_t*)packed, cin, cout); break;
+    case 4: launch_k(pack_pw_kernel<uint32_t>, dim3(grid), dim3(block), 0, st, (const uint32_t*)w, (uint32_t*)packed, cin, cout); break;
+    case 2: launch_k(pack_pw_kernel<uint16_t>, dim3(grid), dim3(block), 0, st, (const uint16_t*)w, (uint16_t*)packed, cin, cout); break;
+    default: launch_k(pack_pw_kernel<uint8_t>, dim3(grid), dim3(block), 0, st, (const uint8_t*)w, (uint8_t*)packed, cin, cout); break;
   }
   return check_launch("pack_pw_kernel");
 }

@@ -47,6 +47,13 @@ __device__ __forceinline__ void stg64(void* p, uint32_t x, uint32_t y) {
   asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(x), "r"(y) : "memory");
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel lets its successor launch early (its CTAs start on SMs this grid has left and run
+// their prologue: barrier init, TMEM alloc, weight / constant staging) and waits for the previous
+// grid to complete before touching activations (reads of its output, writes of its input).
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -142,6 +149,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 // ------------------------------------------------------------------ named barriers
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ------------------------------------------------------------------ tcgen05

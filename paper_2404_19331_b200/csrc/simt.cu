@@ -41,6 +41,8 @@ template <int DT>
 __global__ void __launch_bounds__(256) pw_simt_kernel(const typename Tr<DT>::T* __restrict__ x,
                                                       const typename Tr<DT>::T* __restrict__ wp, Epi ep,
                                                       typename Tr<DT>::T* __restrict__ y, int M, int K, int N) {
+  pdl_launch();
+  pdl_wait();
   using A = typename Tr<DT>::acc_t;
   __shared__ A xs[16][64 + 4];
   __shared__ A ws[16][64 + 4];
@@ -102,6 +104,8 @@ template <int DT>
 __global__ void dw_nhwc_simt_kernel(const typename Tr<DT>::T* __restrict__ x, const typename Tr<DT>::T* __restrict__ wdw,
                                     Epi ep, typename Tr<DT>::T* __restrict__ y, int H, int W, int C, int Ho, int Wo,
                                     int k, int s, int pt, int pl, long long total) {
+  pdl_launch();
+  pdl_wait();
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int c = idx % C;
@@ -125,6 +129,8 @@ __global__ void __launch_bounds__(256) dwpw_simt_kernel(const typename Tr<DT>::T
                                                         typename Tr<DT>::T* __restrict__ y, int N, int H, int W, int C,
                                                         int Ho, int Wo, int Cout, int k, int s, int pt, int pl,
                                                         int tiles_x, int tiles_y) {
+  pdl_launch();
+  pdl_wait();
   using A = typename Tr<DT>::acc_t;
   __shared__ A ts[32][64 + 4];
   __shared__ A ws[32][64 + 4];
@@ -187,6 +193,8 @@ __global__ void __launch_bounds__(256) pwdw_simt_kernel(const typename Tr<DT>::T
                                                         typename Tr<DT>::T* __restrict__ y, int N, int H, int W, int C,
                                                         int Ho, int Wo, int Cmid, int k, int s, int pt, int pl,
                                                         int tiles_x, int tiles_y) {
+  pdl_launch();
+  pdl_wait();
   using A = typename Tr<DT>::acc_t;
   extern __shared__ __align__(16) unsigned char tsm_raw[];  // [R][33] acc_t
   A* tsm = reinterpret_cast<A*>(tsm_raw);
@@ -243,7 +251,7 @@ int launch_pw_simt(int dt, const void* x, const void* wp, const Epi& ep, void* y
                    cudaStream_t st) {
   dim3 grid((M + 63) / 64, (N + 63) / 64);
 #define L_PW(D)                                                                                       \
-  (pw_simt_kernel<D><<<grid, 256, 0, st>>>(static_cast<const Tr<D>::T*>(x), static_cast<const Tr<D>::T*>(wp), ep, \
+  (launch_k(pw_simt_kernel<D>, dim3(grid), dim3(256), 0, st, static_cast<const Tr<D>::T*>(x), static_cast<const Tr<D>::T*>(wp), ep, \
                                            static_cast<Tr<D>::T*>(y), M, K, N),                       \
    check_launch("pw_simt_kernel"))
   FCM_DT_SWITCH(dt, L_PW)
@@ -254,7 +262,7 @@ int launch_dw_simt(int dt, const void* x, const void* wdw, const Epi& ep, void* 
   const long long total = (long long)g.N * g.Ho * g.Wo * g.C;
   const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)device_props().sms * 16);
 #define L_DW(D)                                                                                            \
-  (dw_nhwc_simt_kernel<D><<<blocks, 256, 0, st>>>(static_cast<const Tr<D>::T*>(x), static_cast<const Tr<D>::T*>(wdw), \
+  (launch_k(dw_nhwc_simt_kernel<D>, dim3(blocks), dim3(256), 0, st, static_cast<const Tr<D>::T*>(x), static_cast<const Tr<D>::T*>(wdw), \
                                                    ep, static_cast<Tr<D>::T*>(y), g.H, g.W, g.C, g.Ho, g.Wo, g.k, g.s,  \
                                                    g.pt, g.pl, total),                                     \
    check_launch("dw_nhwc_simt_kernel"))
@@ -267,7 +275,7 @@ int launch_dwpw_simt(int dt, const void* x, const void* wdw, const Epi& ed, cons
   const int tiles_x = (g.Wo + 7) / 8, tiles_y = (g.Ho + 7) / 8;
   dim3 grid(tiles_x * tiles_y * g.N, (g.Cout + 63) / 64);
 #define L_DWPW(D)                                                                                          \
-  (dwpw_simt_kernel<D><<<grid, 256, 0, st>>>(static_cast<const Tr<D>::T*>(x), static_cast<const Tr<D>::T*>(wdw), ed, \
+  (launch_k(dwpw_simt_kernel<D>, dim3(grid), dim3(256), 0, st, static_cast<const Tr<D>::T*>(x), static_cast<const Tr<D>::T*>(wdw), ed, \
                                              static_cast<const Tr<D>::T*>(wp), ep, static_cast<Tr<D>::T*>(y), g.N, g.H,   \
                                              g.W, g.C, g.Ho, g.Wo, g.Cout, g.k, g.s, g.pt, g.pl, tiles_x, tiles_y),  \
    check_launch("dwpw_simt_kernel"))
@@ -285,7 +293,7 @@ static int launch_pwdw_simt_t(const void* x, const void* wp, const Epi& ep, cons
     cudaFuncSetAttribute(pwdw_simt_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(tiles_x * tiles_y * g.N, (g.Cout + 31) / 32);
   using TT = typename Tr<DT>::T;
-  pwdw_simt_kernel<DT><<<grid, 256, smem, st>>>(static_cast<const TT*>(x), static_cast<const TT*>(wp), ep,
+  launch_k(pwdw_simt_kernel<DT>, dim3(grid), dim3(256), smem, st, static_cast<const TT*>(x), static_cast<const TT*>(wp), ep,
                                                 static_cast<const TT*>(wdw), ed, static_cast<TT*>(y), g.N, g.H, g.W,
                                                 g.C, g.Ho, g.Wo, g.Cout, g.k, g.s, g.pt, g.pl, tiles_x, tiles_y);
   return check_launch("pwdw_simt_kernel");

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(576, 1)
     pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                  const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, FDiv fnbn,
                  int stages, int ng, uint32_t tmem_cols, int ncap, int resB, unsigned long long* trace, int dbg) {
+  pdl_launch();
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(576, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // previous kernel's outputs (our inputs) complete; our outputs free to overwrite
   const uint32_t tbase = *tslot;
   const int nbm = (M + 127) / 128;
   const int total = nbm * nbn;
@@ -346,19 +348,24 @@ template <int DT, int K> constexpr int dwpw_wbytes(int nk) {
 }
 
 template <int DT, int K, int S>
-__global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
+__global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     dwpw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
                    void* __restrict__ tmy_base, const typename Tr<DT>::T* __restrict__ wdw, Epi ed,
                    Epi ep, int N, int Cin, int Ho, int Wo, int Cout, int pt, int pl, int nb, int th, int tw,
                    int tiles_x, int tiles_y, int nsplit, int BN, int XS, int BS, uint32_t tmem_cols, int ncap, int resB,
                    DwDivs dv, int na, int nacc, int MB, int albo, int dbg, unsigned long long* trace) {
+  pdl_launch();
   constexpr int V = Tr<DT>::VEC;
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
   constexpr int KSTEP = 32 / Tr<DT>::ES;
   constexpr int kDwpwNDW = dwpw_ndw<DT, K>();
-  constexpr int WARP_TX = 4 + kDwpwNDW, WARP_TB = 5 + kDwpwNDW, WARP_MMA = 6 + kDwpwNDW;
+  constexpr int WARP_TX = 4 + kDwpwNDW, WARP_TB = 5 + kDwpwNDW, WARP_MMA = 6 + kDwpwNDW, WARP_RELAY = 7 + kDwpwNDW;
+  // relay: one warp turns "X stage landed (TMA mbarrier) and A slot free (MMA commit mbarrier)"
+  // into a named-barrier release of the DW warps (bar.sync ~ tens of cycles vs ~200 per
+  // mbarrier try_wait round trip on the DW warps' critical path); barriers 2/3 alternate phases
+  constexpr uint32_t kGoThreads = (kDwpwNDW + 1) * 32;
   const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
   const int xbytes = nb * th_in * tw_in * 128;
   const int xstride = (xbytes + 1023) & ~1023;
@@ -404,6 +411,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // previous kernel's outputs (our inputs) complete; our outputs free to overwrite
   const uint32_t tbase = *tslot;
   const int spatial = ((N + nb - 1) / nb) * tiles_y * tiles_x;
   const int total = spatial * nsplit;
@@ -497,6 +505,15 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
         stamp(local, 2);
       }
     }
+  } else if (warp == WARP_RELAY) {
+    Ring rx(XS), ra(na);
+    int p = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x)
+      for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next(), ++p) {
+        mbar_wait(fullX + rx.i, rx.ph);
+        mbar_wait(aempty + ra.i, ra.ph ^ 1);
+        named_bar_arrive(2 + (p & 1), kGoThreads);
+      }
   } else if (warp >= 4) {
     // ---------------- DW warps: X halo chunk (smem) -> DW -> eps_dw -> A operand (commBuffer)
     constexpr int kSeg = 8;
@@ -507,9 +524,9 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
     uint64_t W9[9], bias2 = 0ull;
     int kc_w = -1;
     Ring rx(XS), ra(na);
-    int local = 0;
+    int local = 0, phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next()) {
+      for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next(), ++phase) {
         const int sx = rx.i, a = ra.i;
         const int c = kc * KC + lane * V;
         const uint32_t st = smem_u32(xbuf + sx * xstride);
@@ -533,9 +550,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
           const int hp = (tw + 1) >> 1;   // column pairs per image row
           const int ncp = nb * hp;
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 10);
-          mbar_wait(fullX + sx, rx.ph);
-          if (dw == 0 && lane == 0 && kc == 0) stamp(local, 6);
-          if (!(dbg & 128)) mbar_wait(aempty + a, ra.ph ^ 1);
+          named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 11);
           // item = (column pair, segment of SEG rows); SEG chosen on the host per lane-group width
           auto run_items = [&](auto segc, auto actc, FDiv fnsg) {
@@ -579,8 +594,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 3) * 32, 1)
           EpiC ec[V];
 #pragma unroll
           for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
-          mbar_wait(fullX + sx, rx.ph);
-          mbar_wait(aempty + a, ra.ph ^ 1);
+          named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
           for (int item = dw; item < nitems; item += kDwpwNDW) {
             const int col = item / nseg, seg = item - col * nseg;
             const int b = col / tw, x = col - b * tw;
@@ -699,6 +713,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
                    int W, int Cin, int Ho, int Wo, int Cmid, int pt, int pl, int nb, int th, int tw, int tiles_x,
                    int tiles_y, int stages, int depth, uint32_t tmem_cols, int ncap, int resB, PwdwDivs dv,
                    int dbg, unsigned long long* trace) {
+  pdl_launch();
   constexpr int ES = Tr<DT>::ES;
   constexpr int V = Tr<DT>::VEC;
   constexpr int KC = 128 / ES;
@@ -756,6 +771,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // previous kernel's outputs (our inputs) complete; our outputs free to overwrite
   const uint32_t tbase = *tslot;
   const int spatial = ((N + nb - 1) / nb) * tiles_y * tiles_x;
   const int total = spatial * nslice;
@@ -1089,7 +1105,7 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   while (ng > 1 && 2 * ng * BN > 512) ng /= 2;
   auto kern = pw_tc_kernel<DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, 576, smem, st>>>(ta, tb, ty, ep, M, N, K, BN, nbn, make_fdiv(nbn), stages, ng, pow2_cols(2 * ng * BN),
+  launch_k(kern, dim3(grid), dim3(576), smem, st, ta, tb, ty, ep, M, N, K, BN, nbn, make_fdiv(nbn), stages, ng, pow2_cols(2 * ng * BN),
                                 ncap, resB ? 1 : 0, trace_buf(), debug_flags());
   const int rc = check_launch("pw_tc_kernel");
   trace_dump("pw");
@@ -1190,7 +1206,7 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   using TT = typename Tr<DT>::T;
   DwDivs dv = dwpw_divs<K, S>(g, dwpw_ndw<DT, K>(), nsplit);
-  kern<<<grid, (4 + dwpw_ndw<DT, K>() + 3) * 32, smem, st>>>(tx, tb, y, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
+  launch_k(kern, dim3(grid), dim3((4 + dwpw_ndw<DT, K>() + 4) * 32), smem, st, tx, tb, y, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
                                                               g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw,
                                                               tiles_x, tiles_y, nsplit, BN, XS, BS,
                                                               pow2_cols(nacc * MB * BN), ncap, resB ? 1 : 0, dv, na,
@@ -1296,7 +1312,7 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   auto kern = pwdw_tc_kernel<DT, K, S>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   using TT = typename Tr<DT>::T;
-  kern<<<grid, (pwdw_ntp<K>() + kPwdwNDW + 2) * 32, smem, st>>>(tx, tb, static_cast<const TT*>(wdw), ep, ed,
+  launch_k(kern, dim3(grid), dim3((pwdw_ntp<K>() + kPwdwNDW + 2) * 32), smem, st, tx, tb, static_cast<const TT*>(wdw), ep, ed,
                                                      static_cast<uint8_t*>(y), g.N, g.H, g.W, g.C, g.Ho, g.Wo, g.Cout,
                                                      g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages, dep,
                                                      pow2_cols(dep * MB * TD), ncap, resB ? 1 : 0,
