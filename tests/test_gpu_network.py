@@ -1,0 +1,62 @@
+"""Whole DW/PW stacks on the GPU through the C ABI (MobileNetV2 / EfficientNet-B0, synthetic).
+
+* int8: FCMs are bit-exact with the unfused composition (reading R2), so a FusePlanner plan and
+  the all-LBL plan of the same stack must give identical bytes.
+* Programmatic dependent launch (FCM_PDL) changes only launch overlap, never results: the
+  bf16 stack output is bitwise identical with it on and off (separate processes: the switch is
+  read once per process).
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lbl_plan(plan):
+    ents = [dict(e) for e in plan["candidates"]["lbl"]]
+    return {"entries": ents, "totals": plan["totals"], "mode": plan["mode"]}
+
+
+@pytest.mark.parametrize("net,dt,batch", [("efficientnet_b0", "s8", 3), ("mobilenet_v1", "s8", 2)])
+def test_int8_stack_fused_plan_equals_layer_by_layer(net, dt, batch):
+    import paper_2404_19331_b200 as fcm
+    from paper_2404_19331_b200.network import Network, model_json
+    plan = fcm.plan(model_json(net, dt, batch))
+    assert plan["totals"]["fused_pairs"] > 0
+    a = Network(net, dt, batch, plan)
+    a.run()
+    b = Network(net, dt, batch, _lbl_plan(plan))
+    b.run()
+    torch.cuda.synchronize()
+    assert torch.equal(a.out.cpu(), b.out.cpu())
+
+
+_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_2404_19331_b200 as fcm
+from paper_2404_19331_b200.network import Network, model_json
+plan = fcm.plan(model_json("mobilenet_v2", "bf16", 4))
+n = Network("mobilenet_v2", "bf16", 4, plan)
+g = n.capture()
+g.replay(); g.replay()
+torch.cuda.synchronize()
+torch.save(n.out.cpu(), sys.argv[1])
+"""
+
+
+def test_pdl_does_not_change_results(tmp_path):
+    outs = []
+    for pdl in ("0", "1"):
+        f = tmp_path / f"out{pdl}.pt"
+        env = dict(os.environ, FCM_PDL=pdl)
+        r = subprocess.run([sys.executable, "-c", _SCRIPT.format(root=ROOT), str(f)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(torch.load(f))
+    assert torch.equal(outs[0], outs[1])

@@ -103,3 +103,22 @@ def test_mobilenet_v2_fuses_every_block_and_saves_bytes(fcm):
     # compulsory bytes: 6605.1 MB LBL -> 2774.1 MB fused
     assert p["totals"]["lbl_dram_bytes"] == 6605130944
     assert p["totals"]["dram_bytes"] == 2774092992
+
+
+@pytest.mark.parametrize("dt", ["bf16", "s8"])
+def test_dwpw_tiles_respect_mma_rows_and_tmem(fcm, dt):
+    # the bf16/f16 3x3 pair core takes tiles of up to 256 pixels (two M=128 MMA row blocks) when
+    # 2 x 2 x C_out fits 512 TMEM columns; every other DWPW tile stays within one 128-row block
+    p = fcm.plan(model_json("mobilenet_v2", dt, 256))
+    net = {l["id"]: l for l in model_json("mobilenet_v2", dt, 256)["layers"]}
+    big = 0
+    for c in p["candidates"]["fcm"]:
+        if c["op"] != "dwpw":
+            continue
+        t = c["tile"]
+        px = t["tile_n"] * t["tile_h"] * t["tile_w"]
+        cout = net[c["layers"][1]]["c_out"]
+        limit = 256 if (dt == "bf16" and cout <= 128) else 128
+        assert 0 < px <= limit, (c["layers"], t)
+        big += px > 128
+    assert (big > 0) == (dt == "bf16")
