@@ -25,6 +25,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fused DW+PW layer µs & HBM GB/s vs B200 peak; MobileNetV2 images/sec @1/2/4/8"
+# BASELINE.json configs index of each network's stack (configs[0] is the single-layer parity case)
+CONFIG_OF = {"single_dwpw": "configs[0]", "mobilenet_v1": "configs[1]", "mobilenet_v2": "configs[2]",
+             "efficientnet_b0": "configs[3]", "cvt13": "configs[4]"}
 DTYPE_NAME = {"bf16": "bf16", "f16": "f16", "s8": "s8", "f32": "f32"}
 
 
@@ -399,7 +402,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded splitmix64 inputs/weights, random-init)",
-            "config": {"workload": f"{args.net} DW/PW stack (configs[2]), {args.batch} img/GPU, 224x224",
+            "config": {"workload": f"{args.net} DW/PW stack ({CONFIG_OF.get(args.net, 'not a BASELINE config')}), "
+                                   f"{args.batch} img/GPU, 224x224",
                        "net": args.net, "global_batch": ws * args.batch, "plan_mode": plan["mode"],
                        "fused_pairs": plan["totals"]["fused_pairs"], "kernels_per_step": launches_per_step,
                        "parallelism": f"batch-sharded x{ws} (replicas, no collective on the hot path)",

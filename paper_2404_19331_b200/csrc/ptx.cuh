@@ -98,6 +98,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // Wait for a phase that is usually far away (roles with little work per tile): back off with
 // nanosleep between polls so idle warps do not steal issue slots from the compute warps.
+template <uint32_t kMaxNs = 256>
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
@@ -105,7 +106,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   uint32_t ns = 32;
   while (!done) {
     __nanosleep(ns);
-    ns = ns < 256 ? ns * 2 : 256;
+    ns = ns < kMaxNs ? ns * 2 : kMaxNs;
     asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
                  : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   }

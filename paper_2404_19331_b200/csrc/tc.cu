@@ -193,7 +193,8 @@ template <int DT>
 __global__ void __launch_bounds__(576, 1)
     pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                  const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, FDiv fnbn,
-                 int stages, int ng, uint32_t tmem_cols, int ncap, int resB, unsigned long long* trace, int dbg) {
+                 int stages, int ng, int nbuf, uint32_t tmem_cols, int ncap, int resB, unsigned long long* trace,
+                 int dbg) {
   pdl_launch();
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(576, 1)
     tma_prefetch_desc(&tmb);
     tma_prefetch_desc(&tmy);
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2 * ng; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4 * spg); }
+    for (int a = 0; a < nbuf * ng; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4 * spg); }
     mbar_init(bfull, 1);
     fence_barrier_init();
   }
@@ -235,11 +236,11 @@ __global__ void __launch_bounds__(576, 1)
   auto stamp = [&](int local, int ev) {
     if (trace && blockIdx.x == 0 && local < 64) trace[local * 16 + ev] = clock64();
   };
-  // tile l of this CTA -> accumulator (group l % ng, alternate buffers) and its phase
+  // tile l of this CTA -> accumulator (group l % ng, its nbuf buffers in turn) and its phase
   auto acc_of = [&](int l, int& acc, uint32_t& ph) {
     const int g = l % ng, j = l / ng;
-    acc = 2 * g + (j & 1);
-    ph = (j >> 1) & 1;
+    acc = nbuf * g + (nbuf == 2 ? (j & 1) : 0);
+    ph = (nbuf == 2 ? (j >> 1) : j) & 1;
   };
 
   if (warp == 16) {
@@ -447,6 +448,10 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           mbar_wait(emptyX + rx.i, rx.ph ^ 1);
           if (kc == 0) stamp(local, 8);
           if (kc == nk - 1) stamp(local, 9);
+          if (dbg & 8) {  // development: skip the X load (timing attribution only)
+            mbar_arrive(fullX + rx.i);
+            continue;
+          }
           mbar_arrive_expect_tx(fullX + rx.i, xbytes);
           tma_load_4d(xbuf + rx.i * xstride, &tmx, fullX + rx.i, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
         }
@@ -1099,13 +1104,18 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   }
   // epilogue groups: 4 x nch warps per tile, so 4 / nch tiles can drain concurrently (2 TMEM
   // accumulators per group)
+  // 3 chunks: two groups (slots of 2 warps per quadrant, 2 + 1 chunks) with one accumulator each;
+  // the MMA still alternates between two accumulators (one per group)
   const int nchk = (BN * Tr<DT>::ES + 127) / 128;
   int ng = nchk >= 4 ? 1 : 4 / nchk;
   if (ng == 3) ng = 2;
-  while (ng > 1 && 2 * ng * BN > 512) ng /= 2;
+  int nbuf = 2;
+  if (nchk == 3 && 2 * BN <= 512) { ng = 2; nbuf = 1; }
+  while (ng > 1 && nbuf * ng * BN > 512) ng /= 2;
   auto kern = pw_tc_kernel<DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_k(kern, dim3(grid), dim3(576), smem, st, ta, tb, ty, ep, M, N, K, BN, nbn, make_fdiv(nbn), stages, ng, pow2_cols(2 * ng * BN),
+  launch_k(kern, dim3(grid), dim3(576), smem, st, ta, tb, ty, ep, M, N, K, BN, nbn, make_fdiv(nbn), stages, ng, nbuf,
+           pow2_cols(nbuf * ng * BN),
                                 ncap, resB ? 1 : 0, trace_buf(), debug_flags());
   const int rc = check_launch("pw_tc_kernel");
   trace_dump("pw");
