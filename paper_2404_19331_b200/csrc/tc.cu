@@ -765,9 +765,11 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
     for (int a = 0; a < depth; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, NTP);  // one arrive per warp (after __syncwarp)
-      mbar_init(Tfull + a, NTP);
-      mbar_init(Tempty + a, kPwdwNDW);
+      mbar_init(tempty + a, NTP);  // one arrive per warp (after __syncwarp): TMEM reads only
+      // the T tile (generic-proxy smem written by the producers, read by the DW consumers) is handed
+      // over with every thread's own arrive: an explicit release by each writer / reader
+      mbar_init(Tfull + a, NTP * 32);
+      mbar_init(Tempty + a, kPwdwNDW * 32);
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -893,11 +895,9 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
         }
       }
       tc_fence_before();
+      mbar_arrive(Tfull + acc);
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(tempty + acc);
-        mbar_arrive(Tfull + acc);
-      }
+      if (lane == 0) mbar_arrive(tempty + acc);
       if (warp == 0 && lane == 0) stamp(local, 5);
     }
   } else {
@@ -990,8 +990,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
                                });
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(Tempty + tbi);
+      mbar_arrive(Tempty + tbi);
       if (dw == 0 && lane == 0) stamp(local, 7);
     }
   }

@@ -10,6 +10,11 @@ for args, kw in [(("dw", "bf16", 1, 9, 11, 64), {}), (("dw", "s8", 1, 9, 7, 32),
                  (("dwpw", "bf16", 2, 9, 11, 96, 40), {}), (("dwpw", "s8", 1, 9, 9, 32, 48), {"k": 5, "s": 2}),
                  (("pwdw", "bf16", 2, 9, 11, 24, 72), {}), (("pwdw", "bf16", 1, 12, 12, 24, 72), {"s": 2}),
                  (("pwdw", "s8", 1, 9, 9, 32, 48), {}), (("dwpw", "f32", 1, 9, 9, 16, 32), {}),
-                 (("pwdw", "f32", 1, 9, 9, 16, 32), {})]:
+                 (("pwdw", "f32", 1, 9, 9, 16, 32), {}),
+                 # round-1 paths: two-row-block DWPW tile (pair core, register epilogue), f16 pair
+                 # core, PW epilogue groups (96 columns: 2 groups x 2 buffers; 144: 2 groups x 1)
+                 (("dwpw", "bf16", 2, 18, 20, 64, 40), {"tile": dict(tile_h=16, tile_w=16)}),
+                 (("dwpw", "f16", 1, 15, 13, 24, 16), {"tile": dict(tile_h=14, tile_w=13)}),
+                 (("pw", "bf16", 2, 13, 11, 16, 96), {}), (("pw", "bf16", 2, 13, 11, 24, 144), {})]:
     Case(*args, **kw).check()
     print("ok", args, kw, flush=True)
