@@ -49,7 +49,34 @@ def chain_dp(order, lbl, fcm_cost):
     return sel[::-1], dp[n]
 
 
-def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=False):
+def dwpw_tile_alternatives(tile, ho, wo, k, s, cout, dtype, limit=10):
+    """A few DWPW output tiles besides the planner's (measured, not modelled, choice): row/column
+    extents from {4, 7, 8, 14, 16, 28} that fit the MMA rows (256 for the bf16/f16 3x3 pair core
+    when 2 x 2 x C_out <= 512 TMEM columns, else 128), whole-map tiles with several images."""
+    mmax = 256 if (dtype in ("bf16", "f16") and k == 3 and cout <= 128) else 128
+    out = [dict(tile)]
+    sizes = [4, 7, 8, 14, 16, 28]
+    for th in sizes:
+        for tw in sizes:
+            if th > ho or tw > wo or th * tw > mmax or th * tw < 32 or (s == 2 and th * tw > 128):
+                continue
+            out.append({"tile_n": 1, "tile_h": th, "tile_w": tw, "n_split": tile.get("n_split", 1)})
+    if ho * wo <= mmax // 2:
+        for nb in range(2, mmax // (ho * wo) + 1):
+            out.append({"tile_n": nb, "tile_h": ho, "tile_w": wo, "n_split": tile.get("n_split", 1)})
+    seen, uniq = set(), []
+    for t in out:
+        key = (t["tile_n"], t["tile_h"], t["tile_w"])
+        if key not in seen:
+            seen.add(key)
+            uniq.append(t)
+    # prefer tiles near the planner's pixel count (keeps the search short)
+    px0 = tile["tile_n"] * tile["tile_h"] * tile["tile_w"]
+    rest = sorted(uniq[1:], key=lambda t: abs(t["tile_n"] * t["tile_h"] * t["tile_w"] - px0))
+    return [uniq[0]] + rest[:limit - 1]
+
+
+def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=False, tile_search=True):
     plan = fcm.plan(model_json(net, dtype, batch))
     cands = plan["candidates"]
     # one Network instance whose "plan" is every candidate, so each has real buffers to run on
@@ -63,12 +90,29 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
         cin = l0["c"] if l0["kind"] == "dw" else l0["c_in"]
         src = torch.zeros((batch, l0["h"], l0["w"], cin), dtype=probe.x.dtype, device=device)
         out = torch.empty(probe._out_shape(lids[-1]), dtype=probe.x.dtype, device=device)
-        f = probe._make_call(c, src, out)
-        try:
-            meas[tuple(lids)] = _time(f, reps)
-        except Exception as e:  # infeasible tile etc.: never chosen
-            if verbose:
-                print("skip", lids, e)
+        tiles = [c.get("tile")]
+        if tile_search and c["op"] == "dwpw" and c.get("tile"):
+            d = probe.layers[lids[0]]
+            kk, ss = d["k"], d["stride"]
+            ho = (d["h"] + 2 * (kk // 2) - kk) // ss + 1
+            wo = (d["w"] + 2 * (kk // 2) - kk) // ss + 1
+            tiles = dwpw_tile_alternatives(c["tile"], ho, wo, kk, ss, probe.layers[lids[1]]["c_out"], dtype)
+        best = None
+        for t in tiles:
+            ct = dict(c, tile=t) if t is not None else c
+            f = probe._make_call(ct, src, out)
+            try:
+                us = _time(f, reps)
+            except Exception as e:  # infeasible tile etc.: never chosen
+                if verbose:
+                    print("skip", lids, t, e)
+                continue
+            if best is None or us < best[0]:
+                best = (us, t)
+        if best is not None:
+            meas[tuple(lids)] = best[0]
+            if best[1] is not None:
+                c["tile"] = best[1]
         del src, out
     lbl = {l: meas[(l,)] for l in order}
     fcm_cost = {k: v for k, v in meas.items() if len(k) == 2 and v < lbl[k[0]] + lbl[k[1]]}
