@@ -280,8 +280,16 @@ def main():
     from paper_2404_19331_b200.network import Network, model_json
 
     if args.plan == "measured" and args.mode == "b200":
-        from paper_2404_19331_b200.autotune import refine
-        plan = refine(args.net, args.dtype, args.batch, device=dev)
+        # rank 0 measures; every rank executes the same plan (so the shards are bit-identical to
+        # a one-GPU run of the same plan and the post-timing verification is meaningful)
+        plan = None
+        if rank == 0:
+            from paper_2404_19331_b200.autotune import refine
+            plan = refine(args.net, args.dtype, args.batch, device=dev)
+        if ws > 1:
+            box = [plan]
+            torch.distributed.broadcast_object_list(box, src=0)
+            plan = box[0]
     else:
         plan = fcm.plan(model_json(args.net, args.dtype, args.batch, args.mode))
     if args.plan_out and rank == 0:
