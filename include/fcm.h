@@ -40,6 +40,14 @@
  *   `stream` (a cudaStream_t passed as void*; NULL = legacy default stream) and is
  *   asynchronous; there is no implicit synchronisation. Input and output must not overlap.
  *   Re-entrant and thread-safe.
+ *   Kernels are launched with programmatic stream serialization (programmatic dependent
+ *   launch): a call's kernel may start its prologue (barrier / TMEM setup, weight and epilogue
+ *   constant staging) while the previous kernel on the stream drains, and waits for that kernel
+ *   to complete (griddepcontrol.wait) before it reads activations or writes its output. So
+ *   stream order is preserved for activations; weights and epilogue vectors must not be written
+ *   by the kernel immediately preceding the call on the same stream (synchronise or insert any
+ *   other stream operation in between). Environment FCM_PDL=0 turns this off (plain
+ *   stream-ordered launches).
  *
  * Errors
  *   Every entry point returns FCM_OK (0) or a negative FCM_E_* code; validation is synchronous
@@ -106,7 +114,10 @@ typedef struct {
 
 /* Optional tile override (NULL = the library's default for the shape). Output-space tile
  * tile_h x tile_w pixels of tile_n images; n_split = number of C_out slices (DWPW) or the
- * intermediate-channel slice width td (PWDW_R, as c_chunk). 0 = default for that field. */
+ * intermediate-channel slice width td (PWDW_R, as c_chunk). 0 = default for that field.
+ * DWPW tiles hold at most 256 pixels (two M=128 MMA row blocks) on the bf16/f16 3x3 path and
+ * 128 otherwise; PWDW_R halo tiles at most 256 pixels. A tile whose staging does not fit shared
+ * memory / TMEM returns FCM_E_INFEASIBLE. */
 typedef struct {
   int32_t tile_h, tile_w, tile_n, c_chunk, n_split;
 } fcm_tile;
