@@ -37,23 +37,124 @@ __device__ __forceinline__ typename Tr<DT>::T epi1(typename Tr<DT>::acc_t a, con
 
 // ------------------------------------------------------------------ LBL PW
 // Y[M,N] = eps(X[M,K] . Wp[N,K]^T). 64x64 output tile per CTA, 4x4 per thread, K chunks of 16.
+// VEC (row pitches of X / Wp a multiple of 8 bytes and N a multiple of 4): operands staged with
+// 8-byte loads and the 4 consecutive outputs of a thread written as one vector store, instead
+// of element-wise (byte-wise for int8) global accesses.
 template <int DT>
+__device__ __forceinline__ void store4(typename Tr<DT>::T* y, const typename Tr<DT>::T (&v)[4]) {
+  if constexpr (DT == FCM_S8) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w |= (static_cast<uint32_t>(static_cast<uint8_t>(v[j])) << (8 * j));
+    *reinterpret_cast<uint32_t*>(y) = w;
+  } else if constexpr (DT == FCM_F32) {
+    *reinterpret_cast<float4*>(y) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    uint2 w;
+    w.x = static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&v[0])) |
+          (static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&v[1])) << 16);
+    w.y = static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&v[2])) |
+          (static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&v[3])) << 16);
+    *reinterpret_cast<uint2*>(y) = w;
+  }
+}
+
+// int8 with 8-byte pitches: the K chunk stays packed (4 int8 per word) and every word pair is
+// one __dp4a (4 exact int32 MACs per instruction instead of one IMAD each).
+__device__ __forceinline__ void pw_simt_i8_dp4a(const int8_t* __restrict__ x, const int8_t* __restrict__ wp,
+                                                const Epi& ep, int8_t* __restrict__ y, int M, int K, int N) {
+  __shared__ uint32_t xw[4][64 + 4];
+  __shared__ uint32_t ww[4][64 + 4];
+  const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  int32_t acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    {  // 2 x 64 rows x 2 groups of 8 bytes = 256 loads: one per thread
+      const int i = threadIdx.x;
+      const int which = i >> 7, rem = i & 127, r = rem >> 1, gi = rem & 1, kk = gi * 8;
+      const int row = (which ? n0 : m0) + r;
+      uint2 g = make_uint2(0u, 0u);
+      if (row < (which ? N : M) && k0 + kk < K)
+        g = __ldg(reinterpret_cast<const uint2*>((which ? wp : x) + (size_t)row * K + k0 + kk));
+      uint32_t(*dst)[64 + 4] = which ? ww : xw;
+      dst[2 * gi][r] = g.x;
+      dst[2 * gi + 1][r] = g.y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      int a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = (int)xw[kq][ty * 4 + i]; b[i] = (int)ww[kq][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __dp4a(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const int nb = n0 + tx * 4;
+  if (nb >= N) return;
+  EpiC c[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) c[j] = load_epi<FCM_S8>(ep, nb + j, true);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w |= (static_cast<uint32_t>(requant_i8(acc[i][j], c[j], ep.zp_out, ep.qmin, ep.qmax)) & 0xFFu) << (8 * j);
+    *reinterpret_cast<uint32_t*>(y + (size_t)m * N + nb) = w;
+  }
+}
+
+template <int DT, bool VEC>
 __global__ void __launch_bounds__(256) pw_simt_kernel(const typename Tr<DT>::T* __restrict__ x,
                                                       const typename Tr<DT>::T* __restrict__ wp, Epi ep,
                                                       typename Tr<DT>::T* __restrict__ y, int M, int K, int N) {
   pdl_launch();
   pdl_wait();
+  if constexpr (DT == FCM_S8 && VEC) {
+    pw_simt_i8_dp4a(x, wp, ep, y, M, K, N);
+    return;
+  }
   using A = typename Tr<DT>::acc_t;
+  using TT = typename Tr<DT>::T;
+  constexpr int V = Tr<DT>::VEC;          // elements per 32-bit word
+  constexpr int EPG = 2 * V;              // elements per 8-byte group
   __shared__ A xs[16][64 + 4];
   __shared__ A ws[16][64 + 4];
   const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   A acc[4][4] = {};
   for (int k0 = 0; k0 < K; k0 += 16) {
-    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
-      const int r = i / 16, kk = i % 16;
-      xs[kk][r] = (m0 + r < M && k0 + kk < K) ? to_acc<DT>(x[(size_t)(m0 + r) * K + k0 + kk]) : A(0);
-      ws[kk][r] = (n0 + r < N && k0 + kk < K) ? to_acc<DT>(wp[(size_t)(n0 + r) * K + k0 + kk]) : A(0);
+    if constexpr (VEC) {
+      constexpr int GPR = 16 / EPG;       // 8-byte groups per row of the K chunk
+      for (int i = threadIdx.x; i < 2 * 64 * GPR; i += 256) {
+        const int which = i / (64 * GPR), rem = i - which * 64 * GPR;
+        const int r = rem / GPR, gi = rem - r * GPR, kk = gi * EPG;
+        const int row = (which ? n0 : m0) + r;
+        const bool ok = row < (which ? N : M) && k0 + kk < K;
+        uint2 g = make_uint2(0u, 0u);
+        if (ok) g = __ldg(reinterpret_cast<const uint2*>((which ? wp : x) + (size_t)row * K + k0 + kk));
+        A u0[V], u1[V];
+        Tr<DT>::unpack(g.x, u0);
+        Tr<DT>::unpack(g.y, u1);
+        A(*dst)[64 + 4] = which ? ws : xs;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          dst[kk + e][r] = u0[e];
+          dst[kk + V + e][r] = u1[e];
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+        const int r = i / 16, kk = i % 16;
+        xs[kk][r] = (m0 + r < M && k0 + kk < K) ? to_acc<DT>(x[(size_t)(m0 + r) * K + k0 + kk]) : A(0);
+        ws[kk][r] = (n0 + r < N && k0 + kk < K) ? to_acc<DT>(wp[(size_t)(n0 + r) * K + k0 + kk]) : A(0);
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -68,15 +169,32 @@ __global__ void __launch_bounds__(256) pw_simt_kernel(const typename Tr<DT>::T* 
     }
     __syncthreads();
   }
+  if constexpr (VEC) {
+    const int nb = n0 + tx * 4;
+    if (nb >= N) return;
+    EpiC c[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int n = n0 + tx * 4 + j;
-    if (n >= N) continue;
-    const EpiC c = load_epi<DT>(ep, n, true);
+    for (int j = 0; j < 4; ++j) c[j] = load_epi<DT>(ep, nb + j, true);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int m = m0 + ty * 4 + i;
-      if (m < M) y[(size_t)m * N + n] = epi1<DT>(acc[i][j], c, ep);
+      if (m >= M) continue;
+      TT v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = epi1<DT>(acc[i][j], c[j], ep);
+      store4<DT>(y + (size_t)m * N + nb, v);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      const EpiC c = load_epi<DT>(ep, n, true);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = m0 + ty * 4 + i;
+        if (m < M) y[(size_t)m * N + n] = epi1<DT>(acc[i][j], c, ep);
+      }
     }
   }
 }
@@ -250,9 +368,13 @@ __global__ void __launch_bounds__(256) pwdw_simt_kernel(const typename Tr<DT>::T
 int launch_pw_simt(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N,
                    cudaStream_t st) {
   dim3 grid((M + 63) / 64, (N + 63) / 64);
-#define L_PW(D)                                                                                       \
-  (launch_k(pw_simt_kernel<D>, dim3(grid), dim3(256), 0, st, static_cast<const Tr<D>::T*>(x), static_cast<const Tr<D>::T*>(wp), ep, \
-                                           static_cast<Tr<D>::T*>(y), M, K, N),                       \
+  const int es = elem_size(dt);
+  const bool vec = ((size_t)K * es) % 8 == 0 && N % 4 == 0;
+#define L_PW(D)                                                                                                 \
+  ((vec ? launch_k(pw_simt_kernel<D, true>, dim3(grid), dim3(256), 0, st, static_cast<const Tr<D>::T*>(x),    \
+                   static_cast<const Tr<D>::T*>(wp), ep, static_cast<Tr<D>::T*>(y), M, K, N)                   \
+        : launch_k(pw_simt_kernel<D, false>, dim3(grid), dim3(256), 0, st, static_cast<const Tr<D>::T*>(x),   \
+                   static_cast<const Tr<D>::T*>(wp), ep, static_cast<Tr<D>::T*>(y), M, K, N)),                 \
    check_launch("pw_simt_kernel"))
   FCM_DT_SWITCH(dt, L_PW)
 #undef L_PW
