@@ -41,7 +41,6 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     mbar_arrive_expect_tx(&bar, th_in * tw_in * 128);
     tma_load_4d(xs, &tmx, &bar, c0, tx * tw * S - pl, ty * th * S - pt, n);
   }
-  const int c = c0 + lane * V;
   const int y0 = ty * th, x0 = tx * tw;
   const int nrows = min(th, Ho - y0);
   uint32_t* yw = reinterpret_cast<uint32_t*>(y);
@@ -79,21 +78,28 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     }
     return;
   } else {
+    // lane groups as in the pair core: a channel group with fewer valid words than lanes (e.g.
+    // int8 C = 32 -> 8 words) packs 2 or 4 output columns into one warp instead of idling lanes
+    const int cw_valid = min(32, (C - c0 + V - 1) / V);
+    const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+    const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+    const int cl = c0 + wd * V;
     DwW<DT, K> W;
-    load_dw_weights<DT, K>(W, wdw, C, c);
+    load_dw_weights<DT, K>(W, wdw, C, cl);
     EpiC ec[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ep, c + v, c + v < C);
+    for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ep, cl + v, cl + v < C);
     mbar_wait(&bar, 0);
-    for (int col = warp; col < tw; col += 4) {
+    for (int cb = warp * npix; cb < tw; cb += 4 * npix) {
+      const int col = cb + grp;
       const int x = x0 + col;
-      if (x >= Wo) break;
-      const uint32_t src = smem_u32(xs) + ((col * S) * 32 + lane) * 4;
+      const bool live = col < tw && x < Wo;
+      const uint32_t src = smem_u32(xs) + (((live ? col : cb) * S) * 32 + wd) * 4;
       dw_segment<DT, K, S>(src, 128, tw_in * 128, 0, nrows, th_in - 1, W,
                            [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
-                             if (c < C) {
+                             if (live && cl < C) {
                                const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
-                               yw[(pix * C + c) / V] = epi_pack<DT>(acc, ec, ep);
+                               yw[(pix * C + cl) / V] = epi_pack<DT>(acc, ec, ep);
                              }
                            });
     }
