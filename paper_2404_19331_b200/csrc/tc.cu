@@ -524,7 +524,6 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     constexpr int kSeg = 8;
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
-    const int nitems = nb * tw * nseg;
     const uint32_t hi_c = kPair ? bound2<DT>(act_hi(ed.act)) : 0u;
     uint64_t W9[9], bias2 = 0ull;
     int kc_w = -1;
@@ -533,7 +532,6 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next(), ++phase) {
         const int sx = rx.i, a = ra.i;
-        const int c = kc * KC + lane * V;
         const uint32_t st = smem_u32(xbuf + sx * xstride);
         const uint32_t abase = smem_u32(abuf + a * aslot);
         if constexpr (kPair) {
@@ -595,21 +593,32 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           else run_act(std::integral_constant<int, 4>(), dv.n4);
         } else {
           DwW<DT, K> W;
-          load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + lane);
+          // lane groups (as in the pair core): a partly filled channel chunk packs 2 or 4 output
+          // columns into one warp; lanes past the valid words compute with zero weights and their
+          // (finite) words meet zero PW weight rows, so they never reach the output
+          const int cw_valid = min(32, (Cin - kc * KC + V - 1) / V);
+          const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+          const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+          const int cl = kc * KC + wd * V;
+          load_dw_weights_smem<DT, K>(W, wsm, nk * 32, kc * 32 + wd);
           EpiC ec[V];
 #pragma unroll
-          for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
+          for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, cl + v);
           named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
-          for (int item = dw; item < nitems; item += kDwpwNDW) {
-            const int col = item / nseg, seg = item - col * nseg;
+          const int ncolg = (nb * tw + npix - 1) / npix;
+          for (int item = dw; item < ncolg * nseg; item += kDwpwNDW) {
+            const int cg = item / nseg, seg = item - cg * nseg;
+            const int colr = cg * npix + grp;
+            const bool live = colr < nb * tw;
+            const int col = live ? colr : cg * npix;
             const int b = col / tw, x = col - b * tw;
             const int y0 = seg * kSeg;
-            const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + lane) * 4;
+            const uint32_t src = st + (((b * th_in) * tw_in + x * S) * 32 + wd) * 4;
             dw_segment<DT, K, S>(src, 128, tw_in * 128, y0, min(kSeg, th - y0), th_in - 1, W,
                                  [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
                                    const int m = (b * th + yy) * tw + x;
-                                   const uint32_t word = (c < Cin) ? epi_pack<DT>(acc, ec, ed) : 0u;
-                                   sts32(abase + sw128_off(m, lane), word);
+                                   const uint32_t word = (cl < Cin) ? epi_pack<DT>(acc, ec, ed) : 0u;
+                                   if (live) sts32(abase + sw128_off(m, wd), word);
                                  });
           }
         }
