@@ -341,6 +341,7 @@ struct DwDivs {
   FDiv hp, n8, n7, n4;  // column pairs per image, ceil(th / SEG) for SEG = 8, 7, 4
   FDiv nsplit, tx, ty;  // tile decode
   FDiv thw, tw;         // epilogue: MMA row m -> (image, row, col) of the tile
+  FDiv n14;             // ceil(th / 14)
   int seg_sel;          // SEG per lane-group width: byte g (g = 0, 1, 2 for 32, 16, 8 lanes per slot)
 };
 template <int DT, int K> constexpr bool dwpw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
@@ -588,7 +589,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             else run_items(segc, std::integral_constant<int, 0>(), fnsg);
           };
           const int seg_sel = (dv.seg_sel >> (8 * gi)) & 0xFF;
-          if (seg_sel == 8) run_act(std::integral_constant<int, 8>(), dv.n8);
+          if (seg_sel == 14) run_act(std::integral_constant<int, 14>(), dv.n14);
+          else if (seg_sel == 8) run_act(std::integral_constant<int, 8>(), dv.n8);
           else if (seg_sel == 7) run_act(std::integral_constant<int, 7>(), dv.n7);
           else run_act(std::integral_constant<int, 4>(), dv.n4);
         } else {
@@ -1148,7 +1150,7 @@ static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
   for (int gi = 0; gi < 3; ++gi) {
     const int slots = 1 << gi;
     int best = 0, bcost = 1 << 30;
-    for (int seg : {8, 7, 4}) {
+    for (int seg : {14, 8, 7, 4}) {
       const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
       const int rounds = ((nit + slots - 1) / slots + ndw - 1) / ndw;
       const int cost = rounds * ((seg - 1) * S + K + 2);
@@ -1159,7 +1161,7 @@ static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   return DwDivs{make_fdiv(hp),      make_fdiv((g.th + 7) / 8), make_fdiv((g.th + 6) / 7), make_fdiv((g.th + 3) / 4),
                 make_fdiv(nsplit), make_fdiv(tiles_x),        make_fdiv(tiles_y),        make_fdiv(g.th * g.tw),
-                make_fdiv(g.tw),   sel};
+                make_fdiv(g.tw),   make_fdiv((g.th + 13) / 14), sel};
 }
 
 template <int DT, int K, int S>
