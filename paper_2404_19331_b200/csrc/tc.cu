@@ -424,8 +424,14 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
   __syncthreads();
 #endif
   auto stamp = [&](int local, int ev) {
-#ifdef FCM_TRACE_STAMPS
+#if defined(FCM_TRACE_STAMPS) && !defined(FCM_TRACE_CHUNK)
     if (trace && blockIdx.x == 0 && local < 64) tr_sm[local * 12 + ev] = clock64();
+#endif
+  };
+  // chunk-level variant (FCM_TRACE_CHUNK, tools/trace_chunks.py): one row per C_in-chunk phase
+  auto cstamp = [&](int idx, int ev) {
+#if defined(FCM_TRACE_STAMPS) && defined(FCM_TRACE_CHUNK)
+    if (trace && blockIdx.x == 0 && idx < 64) tr_sm[idx * 12 + ev] = clock64();
 #endif
   };
   // tile t -> (C_out split, image group, tile row, tile col) with host-computed magic divisors
@@ -453,6 +459,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             mbar_arrive(fullX + rx.i);
             continue;
           }
+          cstamp(local * nk + kc, 8);
           mbar_arrive_expect_tx(fullX + rx.i, xbytes);
           tma_load_4d(xbuf + rx.i * xstride, &tmx, fullX + rx.i, kc * KC, txi * tw * S - pl, tyi * th * S - pt, nbi * nb);
         }
@@ -491,6 +498,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
         for (int kc = 0; kc < nk; ++kc, ra.next(), rb.next()) {
           const int a = ra.i, sb = resB ? kc : rb.i;
           mbar_wait(afull + a, ra.ph);
+          cstamp(local * nk + kc, 6);
           if (kc == 0) stamp(local, 1);
           mbar_wait(fullB + sb, resB ? 0 : rb.ph);
           tc_fence_after();
@@ -505,6 +513,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             for (int k = 0; k < ksteps && !(dbg & 256); ++k)
               mma_ss<KIND>(d + h * BN, ad + h * (2048 >> 4) + astep * k, bd + 2 * k, idesc, (kc | k) != 0);
           mma_commit(aempty + a);
+          cstamp(local * nk + kc, 7);
           if (!resB) mma_commit(emptyB + sb);
         }
         mma_commit(tfull + acc);
@@ -517,7 +526,9 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     for (int t = blockIdx.x; t < total; t += gridDim.x)
       for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next(), ++p) {
         mbar_wait(fullX + rx.i, rx.ph);
+        if (lane == 0) cstamp(p, 0);
         mbar_wait(aempty + ra.i, ra.ph ^ 1);
+        if (lane == 0) cstamp(p, 1);
         named_bar_arrive(2 + (p & 1), kGoThreads);
       }
   } else if (warp >= 4) {
@@ -554,7 +565,9 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           const int hp = (tw + 1) >> 1;   // column pairs per image row
           const int ncp = nb * hp;
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 10);
+          if (dw == 0 && lane == 0) cstamp(phase, 2);
           named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
+          if (dw == 0 && lane == 0) cstamp(phase, 3);
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 11);
           // item = (column pair, segment of SEG rows); SEG chosen on the host per lane-group width
           auto run_items = [&](auto segc, auto actc, FDiv fnsg) {
@@ -631,6 +644,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           mbar_arrive(emptyX + sx);
         }
         if (dw == 0 && lane == 0 && kc == nk - 1) stamp(local, 7);
+        if (dw == 0 && lane == 0) cstamp(phase, 4);
+        if (dw == kDwpwNDW - 1 && lane == 0) cstamp(phase, 5);
       }
     }
   } else {
