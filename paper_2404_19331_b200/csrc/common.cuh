@@ -525,10 +525,13 @@ __device__ __forceinline__ void dw3_pair(uint32_t src, int col_bytes, int row_by
     for (int r = 0; r < SEG; ++r) {
       const int i = ii - r * S;  // kernel row of this input row for output row r
       if (i < 0 || i > 2) continue;
+      // tap-outer / column-inner: the two columns' FFMA2s share the weight operand back to back
+      // (operand-reuse cache: fewer register-file reads; each accumulator still sees taps in the
+      // same (i, j) order, so results are unchanged)
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+      for (int j = 0; j < 3; ++j)
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
+        for (int c = 0; c < 2; ++c)
           acc[r][c] = f2_fma(x[c * S + j], W[i * 3 + j], (i == 0 && j == 0) ? bias : acc[r][c]);
       if (i == 2) sink(r, acc[r][0], acc[r][1]);
     }
