@@ -150,7 +150,7 @@ __global__ void dw_nchw_kernel(const typename Tr<DT>::T* __restrict__ x, const t
 // Offline PW packing: canonical [C_in][C_out] -> K-major [C_out][C_in].
 template <typename TT>
 __global__ void pack_pw_kernel(const TT* __restrict__ w, TT* __restrict__ p, int cin, int cout) {
-  pdl_launch();
+  // no early trigger: weights are what a following libfcm kernel may stage before its own PDL wait
   pdl_wait();
   __shared__ TT tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx over cout, by over cin
