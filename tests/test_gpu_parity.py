@@ -160,3 +160,35 @@ def test_unaligned_pitch_layers(fmt):
     Case("pw", fmt, 2, 9, 7, 144, 40 if fmt == "s8" else 12).check()
     Case("dwpw", fmt, 2, 14, 14, 240 if fmt == "s8" else 36, 40 if fmt == "s8" else 12, k=5, s=1).check()
     Case("pwdw", fmt, 2, 15, 13, 24 if fmt == "s8" else 12, 144 if fmt == "s8" else 36, k=5, s=2).check()
+
+
+# ---------------------------------------------------------------- round-1 kernel variants
+@pytest.mark.parametrize("fmt", ["bf16", "f16", "s8"])
+@pytest.mark.parametrize("c_out", [16, 96, 144, 192, 320])
+def test_pw_epilogue_groups(fmt, c_out):
+    # 128-byte column chunks per tile: 1 (4 epilogue groups), 2 (2 groups x 2 accumulators),
+    # 3 (2 groups x 1 accumulator, 2 + 1 chunks), >= 4 (1 group); M spans several 128-row tiles
+    Case("pw", fmt, 3, 17, 13, 64 if fmt != "s8" else 128, c_out).check()
+
+
+@pytest.mark.parametrize("fmt,c", [("s8", 32), ("s8", 16), ("bf16", 24), ("bf16", 16), ("f32", 8), ("f16", 40)])
+@pytest.mark.parametrize("s", [1, 2])
+def test_dw_lane_groups_partial_channel_groups(fmt, c, s):
+    # a 128-byte channel group with 8 or 16 valid words: 2-4 output columns per warp
+    Case("dw", fmt, 2, 21, 19, c, k=3, s=s).check()
+
+
+@pytest.mark.parametrize("fmt,c_in,c_out", [("s8", 24, 40), ("s8", 40, 24), ("s8", 24, 36), ("bf16", 12, 36),
+                                            ("f32", 7, 9), ("f32", 16, 12), ("bf16", 6, 10)])
+def test_pw_simt_vector_and_scalar_paths(fmt, c_in, c_out):
+    # pitches TMA cannot address: 8-byte staging + vector stores (int8 via __dp4a) when the row
+    # pitch is a multiple of 8 bytes and C_out of 4, element-wise otherwise
+    Case("pw", fmt, 2, 15, 13, c_in, c_out).check()
+
+
+@pytest.mark.parametrize("fmt", ["s8", "f16"])
+def test_dwpw_lane_groups_non_pair_path(fmt):
+    # int8 3x3 / fp16 5x5 DWPW with partly filled C_in chunks (lane groups in the non-pair DW warps)
+    k = 3 if fmt == "s8" else 5
+    Case("dwpw", fmt, 2, 17, 15, 160 if fmt == "s8" else 72, 48, k=k, s=1).check()
+    Case("dwpw", fmt, 2, 17, 15, 32, 48, k=k, s=2).check()
