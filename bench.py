@@ -236,8 +236,12 @@ def run_reference(args, ws, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
-            "data": "synthetic", "config": {"workload": f"{args.net} DW/PW stack", "net": args.net,
-                                            "images_per_step": per_step},
+            "data": "synthetic", "config": {"workload": f"{args.net} DW/PW stack "
+                                                        f"({CONFIG_OF.get(args.net, 'not a BASELINE config')}), "
+                                                        f"{args.batch} img/GPU, 224x224",
+                                            "net": args.net, "global_batch": ws * args.batch,
+                                            "images_per_step": per_step,
+                                            "sample": "the oracle processes a bounded sample of the batch per step"},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
