@@ -9,6 +9,7 @@
  *   fcm_dwpw    FCM DWPW: DW -> on-chip commBuffer -> PW          (Listing 1)
  *   fcm_pwdw_r  FCM PWDW_R: PW over the halo tile (recomputed) -> on-chip -> DW
  *               (PWDW without redundancy is the full-map tile of the same call)
+ *   fcm_pwpw    FCM PWPW: PW -> on-chip T -> PW
  *   fcm_pack_pw offline PW weight packing ("weight packing is done offline")
  *   fcm_plan    FusePlanner re-parameterised for B200
  *
@@ -21,7 +22,7 @@
  *   eps (int8)      r = ((acc + bias_q[c]) * mult_q[c] + 2^(shift_q[c]-1)) >> shift_q[c]
  *                     (64-bit product, arithmetic shift) + zp_out, clamped to [qmin, qmax].
  *                     acc = sum (q - zp_in) * w, int32. RELU/RELU6 are encoded by qmin/qmax.
- *   DWPW  = PW(DW(X)); PWDW_R = DW(PW(X)). The intermediate T is rounded/requantised to the
+ *   DWPW  = PW(DW(X)); PWDW_R = DW(PW(X)); PWPW = PW2(PW1(X)). The intermediate T is rounded/requantised to the
  *   feature-map dtype but never exists in global memory; the DW of PWDW_R
  *   zero-pads T itself (an out-of-image T tap is 0 / the zero point, not eps_pw(PW(0))).
  *
@@ -141,6 +142,14 @@ int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, con
 int fcm_pwdw_r(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep_pw, const void* w_dw,
                const fcm_dw_geom* geom, const fcm_epilogue* ep_dw, fcm_tensor* y, const fcm_tile* tile,
                void* stream);
+
+/* FCM PWPW: y = PW2(PW1(x)). x [N,H,W,C_in], w1_packed (C_in -> c_mid), w2_packed (c_mid -> C_out),
+ * y [N,H,W,C_out]; T = eps1(x . W1) is rounded / requantised to the feature-map dtype and stays in
+ * shared memory (one 128-pixel tile at a time). Tensor-core path only: bf16 / f16 / int8, c_mid <=
+ * 128, 16-byte pixel pitches for x, T and y (otherwise FCM_E_UNSUPPORTED: run two fcm_pw calls).
+ * For int8, ep2->zp_in must equal ep1->zp_out. `tile` is reserved (pass NULL). */
+int fcm_pwpw(const fcm_tensor* x, const void* w1_packed, int32_t c_mid, const fcm_epilogue* ep1,
+             const void* w2_packed, const fcm_epilogue* ep2, fcm_tensor* y, const fcm_tile* tile, void* stream);
 
 /* Bytes of the packed PW weight buffer for (dtype, C_in, C_out). 0 on invalid input. */
 size_t fcm_pack_pw_bytes(int32_t dtype, int32_t c_in, int32_t c_out);

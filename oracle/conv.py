@@ -98,6 +98,13 @@ def pwdw(x, w_pw, p_pw, w_dw, stride, pads, p_dw, fmt):
     return dw(t, w_dw, stride, pads, p_dw, fmt)
 
 
+def pwpw(x, w1, p1, w2, p2, fmt):
+    """FCM PWPW = PW2(PW1(X)) (the paper's third FCM kind); T rounded /
+    requantised to the FM dtype like every commBuffer."""
+    t = pw(x, w1, p1, fmt)
+    return pw(t, w2, p2, fmt)
+
+
 # ----------------------------------------------------------------------------------
 # magnitude bound for float tolerances (DESIGN.md reading R10)
 # ----------------------------------------------------------------------------------
@@ -123,3 +130,7 @@ def mag_dwpw(x, w_dw, stride, pads, p_dw, w_pw, p_pw):
 
 def mag_pwdw(x, w_pw, p_pw, w_dw, stride, pads, p_dw):
     return mag_dw(mag_pw(x, w_pw, p_pw), w_dw, stride, pads, p_dw)
+
+
+def mag_pwpw(x, w1, p1, w2, p2):
+    return mag_pw(mag_pw(x, w1, p1), w2, p2)

@@ -131,6 +131,18 @@ def fcm_dwpw(x, w_dw, stride, pads, ep_dw: Epilogue, w_packed, ep_pw: Epilogue, 
     return out
 
 
+def fcm_pwpw(x, w1_packed, ep1: Epilogue, w2_packed, ep2: Epilogue, out=None, tile=None):
+    """FCM PWPW: out = PW2(PW1(x)); the intermediate (w1_packed.shape[0] channels) stays on chip."""
+    lib = L.load()
+    n, h, w, _ = x.shape
+    if out is None:
+        out = torch.empty((n, h, w, w2_packed.shape[0]), dtype=x.dtype, device=x.device)
+    xt, yt, e1, e2, ti = _tensor(x), _tensor(out), ep1.c(), ep2.c(), _tile(tile)
+    L.check(lib.fcm_pwpw(C.byref(xt), _ptr(w1_packed), int(w1_packed.shape[0]), C.byref(e1), _ptr(w2_packed),
+                         C.byref(e2), C.byref(yt), _ref(ti), _stream()), "fcm_pwpw")
+    return out
+
+
 def fcm_pwdw_r(x, w_packed, ep_pw: Epilogue, w_dw, stride, pads, ep_dw: Epilogue, out=None, tile=None):
     lib = L.load()
     n, h, w, _ = x.shape
@@ -166,4 +178,4 @@ def fcm_launch_count() -> int:
 
 
 # short aliases
-dw, pw, dwpw, pwdw_r, pack_pw, plan = fcm_dw, fcm_pw, fcm_dwpw, fcm_pwdw_r, fcm_pack_pw, fcm_plan
+dw, pw, dwpw, pwdw_r, pwpw, pack_pw, plan = fcm_dw, fcm_pw, fcm_dwpw, fcm_pwdw_r, fcm_pwpw, fcm_pack_pw, fcm_plan

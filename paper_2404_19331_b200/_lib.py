@@ -12,7 +12,7 @@ FCM_F32, FCM_BF16, FCM_F16, FCM_S8 = 0, 1, 2, 3
 FCM_NHWC, FCM_NCHW = 0, 1
 ACT_NONE, ACT_RELU, ACT_RELU6 = 0, 1, 2
 
-EXPORTS = ["fcm_dw", "fcm_pw", "fcm_dwpw", "fcm_pwdw_r", "fcm_pack_pw_bytes", "fcm_pack_pw", "fcm_plan",
+EXPORTS = ["fcm_dw", "fcm_pw", "fcm_dwpw", "fcm_pwdw_r", "fcm_pwpw", "fcm_pack_pw_bytes", "fcm_pack_pw", "fcm_plan",
            "fcm_launch_count", "fcm_status_str", "fcm_last_error", "fcm_version"]
 
 
@@ -61,6 +61,7 @@ def load() -> C.CDLL:
     lib.fcm_pw.argtypes = [pt, P, pe, pt, pti, P]
     lib.fcm_dwpw.argtypes = [pt, P, pg, pe, P, pe, pt, pti, P]
     lib.fcm_pwdw_r.argtypes = [pt, P, pe, P, pg, pe, pt, pti, P]
+    lib.fcm_pwpw.argtypes = [pt, P, C.c_int32, pe, P, pe, pt, pti, P]
     lib.fcm_pack_pw_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32]
     lib.fcm_pack_pw_bytes.restype = S
     lib.fcm_pack_pw.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, P, P]
@@ -69,7 +70,7 @@ def load() -> C.CDLL:
     lib.fcm_status_str.argtypes = [I]
     lib.fcm_status_str.restype = C.c_char_p
     lib.fcm_last_error.restype = C.c_char_p
-    for f in ("fcm_dw", "fcm_pw", "fcm_dwpw", "fcm_pwdw_r", "fcm_pack_pw", "fcm_plan", "fcm_version"):
+    for f in ("fcm_dw", "fcm_pw", "fcm_dwpw", "fcm_pwdw_r", "fcm_pwpw", "fcm_pack_pw", "fcm_plan", "fcm_version"):
         getattr(lib, f).restype = I
     _lib = lib
     return lib

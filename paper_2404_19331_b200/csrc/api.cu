@@ -264,6 +264,27 @@ int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, con
   return launch_dwpw_tc(x->dtype, x->data, w_dw, to_epi(ep_dw), w_pw_packed, to_epi(ep_pw), y->data, g, nsplit, st);
 }
 
+int fcm_pwpw(const fcm_tensor* x, const void* w1_packed, int32_t c_mid, const fcm_epilogue* ep1,
+             const void* w2_packed, const fcm_epilogue* ep2, fcm_tensor* y, const fcm_tile* tile, void* stream) {
+  (void)tile;
+  FCM_TRY(check_tensor(x, "x", false));
+  FCM_TRY(check_tensor(y, "y", false));
+  if (!w1_packed || !w2_packed) return set_error(FCM_E_INVAL, "weights NULL");
+  if (x->dtype != y->dtype) return set_error(FCM_E_INVAL, "x/y dtype differ");
+  if (c_mid < 1) return set_error(FCM_E_INVAL, "pwpw: c_mid < 1");
+  FCM_TRY(check_epi(ep1, x->dtype, "ep1"));
+  FCM_TRY(check_epi(ep2, x->dtype, "ep2"));
+  if (x->dtype == FCM_S8 && ep2->zp_in != ep1->zp_out)
+    return set_error(FCM_E_INVAL, "pwpw: ep2.zp_in must equal ep1.zp_out (T's zero point)");
+  if (y->n != x->n || y->h != x->h || y->w != x->w) return set_error(FCM_E_INVAL, "pwpw: y spatial dims mismatch");
+  if (overlaps(x, y)) return set_error(FCM_E_INVAL, "pwpw: x and y overlap");
+  if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y) || ((size_t)c_mid * elem_size(x->dtype)) % 16)
+    return set_error(FCM_E_UNSUPPORTED, "pwpw: tensor-core path needs bf16/f16/int8 and 16-byte pitches of x, T, y");
+  const int M = x->n * x->h * x->w;
+  return launch_pwpw_tc(x->dtype, x->data, w1_packed, to_epi(ep1), w2_packed, to_epi(ep2), y->data, M, x->c, c_mid,
+                        y->c, static_cast<cudaStream_t>(stream));
+}
+
 int fcm_pwdw_r(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep_pw, const void* w_dw,
                const fcm_dw_geom* geom, const fcm_epilogue* ep_dw, fcm_tensor* y, const fcm_tile* tile, void* stream) {
   FCM_TRY(check_tensor(x, "x", false));

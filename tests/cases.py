@@ -86,7 +86,7 @@ class Case:
     """One fused or unfused layer on seeded inputs, both sides."""
 
     def __init__(self, op, fmt, n, h, w, c_in, c_out=None, k=3, s=1, pads=None, seed=synth.SEED, tile=None,
-                 act_dw=synth.ACT_RELU6, act_pw=synth.ACT_NONE):
+                 act_dw=synth.ACT_RELU6, act_pw=synth.ACT_NONE, c_mid=None):
         self.op, self.fmt, self.k, self.s, self.tile = op, fmt, k, s, tile
         self.pads = (k // 2,) * 4 if pads is None else tuple(pads)
         self.x = make_x(seed, fmt, n, h, w, c_in)
@@ -101,6 +101,10 @@ class Case:
         elif op == "pwdw":
             self.pp = layer_params(seed, "pw", "pw", fmt, c_in, c_out, act=synth.ACT_RELU6)
             self.pd = layer_params(seed, "dw", "dw", fmt, c_out, k=k, act=act_dw)
+        elif op == "pwpw":
+            self.c_mid = c_mid
+            self.pp1 = layer_params(seed, "pw1", "pw", fmt, c_in, c_mid, act=act_dw)
+            self.pp2 = layer_params(seed, "pw2", "pw", fmt, c_mid, c_out, act=act_pw)
         else:
             raise ValueError(op)
 
@@ -118,6 +122,9 @@ class Case:
             ref = oc.dwpw(x, self.pd["w"], self.s, self.pads, self.pd, self.pp["w"], self.pp, f)
             mag = None if f == "s8" else oc.mag_dwpw(x, self.pd["w"], self.s, self.pads, self.pd, self.pp["w"],
                                                      self.pp)
+        elif self.op == "pwpw":
+            ref = oc.pwpw(x, self.pp1["w"], self.pp1, self.pp2["w"], self.pp2, f)
+            mag = None if f == "s8" else oc.mag_pwpw(x, self.pp1["w"], self.pp1, self.pp2["w"], self.pp2)
         else:
             ref = oc.pwdw(x, self.pp["w"], self.pp, self.pd["w"], self.s, self.pads, self.pd, f)
             mag = None if f == "s8" else oc.mag_pwdw(x, self.pp["w"], self.pp, self.pd["w"], self.s, self.pads,
@@ -135,7 +142,11 @@ class Case:
         if hasattr(self, "pp"):
             wpk = fcm.pack_pw(stored(self.pp["w"], f).to(dev))
             ep = device_epi(self.pp, f, dev)
-        if self.op == "dw":
+        if self.op == "pwpw":
+            w1 = fcm.pack_pw(stored(self.pp1["w"], f).to(dev))
+            w2 = fcm.pack_pw(stored(self.pp2["w"], f).to(dev))
+            y = fcm.pwpw(x, w1, device_epi(self.pp1, f, dev), w2, device_epi(self.pp2, f, dev))
+        elif self.op == "dw":
             y = fcm.dw(x, wdw, self.s, self.pads, ed, tile=self.tile)
         elif self.op == "pw":
             y = fcm.pw(x, wpk, ep)

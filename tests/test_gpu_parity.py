@@ -192,3 +192,23 @@ def test_dwpw_lane_groups_non_pair_path(fmt):
     k = 3 if fmt == "s8" else 5
     Case("dwpw", fmt, 2, 17, 15, 160 if fmt == "s8" else 72, 48, k=k, s=1).check()
     Case("dwpw", fmt, 2, 17, 15, 32, 48, k=k, s=2).check()
+
+
+# ---------------------------------------------------------------- FCM PWPW
+@pytest.mark.parametrize("fmt", ["bf16", "f16", "s8"])
+@pytest.mark.parametrize("c_in,c_mid,c_out", [(144, 24, 144), (64, 64, 384), (96, 96, 576), (32, 128, 200),
+                                              (576, 96, 24)])
+def test_pwpw(fmt, c_in, c_mid, c_out):
+    # M spans several 128-row tiles plus a ragged tail; C_out in several GEMM2 slices
+    if fmt == "s8" and (c_in % 16 or c_mid % 16 or c_out % 16):
+        pytest.skip("int8 tensor-core path needs 16-byte pitches")
+    Case("pwpw", fmt, 3, 13, 11, c_in, c_out, c_mid=c_mid, act_dw=synth.ACT_RELU6).check()
+
+
+def test_pwpw_unsupported_cases_fail_loudly():
+    import paper_2404_19331_b200 as fcm
+    from paper_2404_19331_b200._lib import FcmError
+    with pytest.raises(FcmError, match="UNSUPPORTED"):
+        Case("pwpw", "f32", 1, 4, 4, 16, 16, c_mid=16).check()
+    with pytest.raises(FcmError, match="UNSUPPORTED"):
+        Case("pwpw", "bf16", 1, 4, 4, 16, 16, c_mid=160).check()

@@ -204,3 +204,41 @@ def test_epilogue_float_rounding_and_act():
     assert out.ravel().tolist() == [6.0, 0.0, 1.75]  # RELU6 clamps 7->6, -1.5->0
     p1 = {"act": 1}
     assert conv.epilogue_float(np.array([1 + 2 ** -9, -2.0]), p1, "bf16").tolist() == [1.0, 0.0]
+
+
+def test_pwpw_factorisation_identity():
+    # PWPW with identity epilogues and no rounding is one 1x1 conv with W1 . W2: checked
+    # against torch's fp64 conv2d with the product weight (a different route than pw(pw(.)))
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (2, 5, 4, 6))
+    w1, w2 = rng.uniform(-1, 1, (6, 9)), rng.uniform(-1, 1, (9, 7))
+    ident = dict(act=0, scale=None, bias=None)
+    got = conv.pwpw(x, w1, ident, w2, ident, "f64")
+    wf = torch.from_numpy(w1 @ w2).t()[:, :, None, None]
+    want = F.conv2d(torch.from_numpy(x).permute(0, 3, 1, 2), wf).permute(0, 2, 3, 1).numpy()
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+    # with a bias and RELU between the two PWs the product form no longer holds -> T is materialised
+    p1 = dict(act=1, scale=None, bias=np.full(9, -0.5))
+    assert not np.allclose(conv.pwpw(x, w1, p1, w2, ident, "f64"), want)
+
+
+def test_pwpw_int8_intermediate_is_requantised():
+    # the int8 commBuffer is requantised before the second PW: brute force with Python ints
+    rng = np.random.default_rng(11)
+    x = rng.integers(-128, 128, (1, 2, 3, 4))
+    w1, w2 = rng.integers(-127, 128, (4, 3)), rng.integers(-127, 128, (3, 5))
+    p1 = dict(act=2, bias_q=np.array([5, -7, 0]), mult_q=np.array([1 << 30] * 3), shift_q=np.array([36] * 3),
+              zp_in=0, zp_out=0, qmin=0, qmax=96)
+    p2 = dict(act=0, bias_q=np.zeros(5, np.int64), mult_q=np.array([1 << 30] * 5), shift_q=np.array([33] * 5),
+              zp_in=0, zp_out=0, qmin=-128, qmax=127)
+    got = conv.pwpw(x, w1, p1, w2, p2, "s8")
+    for n, yy, xx in itertools.product(range(1), range(2), range(3)):
+        t = []
+        for c in range(3):
+            acc = sum(int(x[n, yy, xx, i]) * int(w1[i, c]) for i in range(4)) + int(p1["bias_q"][c])
+            r = (acc * (1 << 30) + (1 << 35)) >> 36
+            t.append(min(max(r, 0), 96))
+        for o in range(5):
+            acc = sum(t[c] * int(w2[c, o]) for c in range(3))
+            r = (acc * (1 << 30) + (1 << 32)) >> 33
+            assert got[n, yy, xx, o] == min(max(r, -128), 127)
