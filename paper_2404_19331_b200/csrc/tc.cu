@@ -1383,14 +1383,17 @@ int launch_pwdw_tc(int dt, const void* x, const void* wp, const Epi& ep, const v
 // the feature-map dtype, for one 128-row tile at a time. T never leaves the CTA: GEMM1
 // accumulates in TMEM, the 4 epilogue warps write T as the SW128 K-major A operand of GEMM2
 // (zero / zero-point padded past C_mid, whose W2 columns are TMA zero fill), GEMM2 runs over
-// C_out slices of BN2 columns. Warps 0-3 epilogues, 4 TMA, 5 MMA. C_mid <= 128.
+// C_out slices of BN2 <= 192 columns into two alternating TMEM accumulators. Warps 0-3 produce T
+// (epilogue 1), warps 4-15 drain GEMM2 (epilogue 2: three warps per lane quadrant), 16 TMA of X / W1,
+// 17 MMA, 18 TMA of W2 (resident when it fits: loaded once per CTA),
+// so T of tile t+1 is produced while the slices of tile t drain. C_mid <= 128.
 // =====================================================================================
 template <int DT>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(608, 1)
     pwpw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb1,
                    const __grid_constant__ CUtensorMap tmb2, const __grid_constant__ CUtensorMap tmy, Epi ep1,
-                   Epi ep2, int M, int K1, int Cmid, int N, int BN1, int BN2, int nbn2, int stages,
-                   uint32_t tmem_cols, int ncap1, int ncap2, int dbg) {
+                   Epi ep2, int M, int K1, int Cmid, int N, int BN1, int BN2, int nbn2, int stages, int w2slots,
+                   int resW2, uint32_t tmem_cols, int ncap1, int ncap2, int dbg) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   constexpr MmaKind KIND = TcKind<DT>::kind;
@@ -1402,49 +1405,48 @@ __global__ void __launch_bounds__(192, 1)
   const int sA = 16384 + BN1 * 128;              // X chunk + W1 chunk per stage
   uint8_t* ring = smem;                          // stages x sA
   uint8_t* tbuf = ring + stages * sA;            // T: nk2 x 16 KB SW128 chunks (128 rows)
-  uint8_t* w2buf = tbuf + nk2 * 16384;           // 2 x BN2 x 128 W2 chunk ring
-  uint8_t* stage = w2buf + 2 * BN2 * 128;        // 4 warps x 4 KB output staging
-  uint8_t* cst1 = stage + 4 * 4096;
+  uint8_t* w2buf = tbuf + nk2 * 16384;           // w2slots x BN2 x 128: W2 chunk ring, or all chunks (resW2)
+  uint8_t* stage = w2buf + w2slots * BN2 * 128;        // 12 epilogue-2 warps x 4 KB output staging
+  uint8_t* cst1 = stage + 12 * 4096;
   uint8_t* cst2 = cst1 + consts_bytes<DT>(ncap1);
   uint64_t* full = reinterpret_cast<uint64_t*>(cst2 + consts_bytes<DT>(ncap2));
   uint64_t* empty = full + stages;
   uint64_t* w2full = empty + stages;
-  uint64_t* w2empty = w2full + 2;
-  uint64_t* acc1full = w2empty + 2;
+  uint64_t* w2empty = w2full + w2slots;
+  uint64_t* acc1full = w2empty + w2slots;
   uint64_t* tready = acc1full + 1;
   uint64_t* tfree = tready + 1;
   uint64_t* acc2full = tfree + 1;
-  uint64_t* acc2empty = acc2full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc2empty + 1);
+  uint64_t* acc2empty = acc2full + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc2empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs1 = stage_consts<DT>(ep1, Cmid, ncap1, cst1);
   const EpiS cs2 = stage_consts<DT>(ep2, N, ncap2, cst2);
-  if (warp == 4 && lane == 0) {
+  if (warp == 16 && lane == 0) {
     tma_prefetch_desc(&tma);
     tma_prefetch_desc(&tmb1);
     tma_prefetch_desc(&tmb2);
     tma_prefetch_desc(&tmy);
     for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(w2full + i, 1); mbar_init(w2empty + i, 1); }
+    for (int i = 0; i < w2slots; ++i) { mbar_init(w2full + i, 1); mbar_init(w2empty + i, 1); }
     mbar_init(acc1full, 1);
     mbar_init(tready, 128);  // every epilogue thread releases its own T writes
     mbar_init(tfree, 1);
-    mbar_init(acc2full, 1);
-    mbar_init(acc2empty, 4);
+    for (int i = 0; i < 2; ++i) { mbar_init(acc2full + i, 1); mbar_init(acc2empty + i, 12); }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc_rt(tslot, tmem_cols);
+  if (warp == 17) tmem_alloc_rt(tslot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   pdl_wait();
   const uint32_t tbase = *tslot;
-  const uint32_t tacc1 = tbase, tacc2 = tbase + 128;  // acc1: <= 128 columns, acc2: BN2 columns
+  const uint32_t tacc1 = tbase, tacc2 = tbase + 128;  // acc1: <= 128 columns, acc2: 2 x BN2 columns
   const int nbm = (M + 127) / 128;
 
-  if (warp == 4) {
+  if (warp == 16) {
     if (lane == 0) {
-      Ring rs(stages), rw(2);
+      Ring rs(stages);
       for (int t = blockIdx.x; t < nbm; t += gridDim.x) {
         for (int kc = 0; kc < nk1; ++kc, rs.next()) {
           mbar_wait(empty + rs.i, rs.ph ^ 1);
@@ -1452,20 +1454,34 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_2d(ring + rs.i * sA, &tma, full + rs.i, kc * KC, t * 128);
           tma_load_2d(ring + rs.i * sA + 16384, &tmb1, full + rs.i, kc * KC, 0);
         }
-        for (int j = 0; j < nbn2; ++j)
-          for (int kc = 0; kc < nk2; ++kc, rw.next()) {
-            mbar_wait(w2empty + rw.i, rw.ph ^ 1);
-            mbar_arrive_expect_tx(w2full + rw.i, BN2 * 128);
-            tma_load_2d(w2buf + rw.i * BN2 * 128, &tmb2, w2full + rw.i, kc * KC, j * BN2);
-          }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 18) {
+    if (lane == 0) {
+      if (resW2) {
+        for (int j = 0; j < nbn2; ++j)
+          for (int kc = 0; kc < nk2; ++kc) {
+            const int sl = j * nk2 + kc;
+            mbar_arrive_expect_tx(w2full + sl, BN2 * 128);
+            tma_load_2d(w2buf + sl * BN2 * 128, &tmb2, w2full + sl, kc * KC, j * BN2);
+          }
+      } else {
+        Ring rw(w2slots);
+        for (int t = blockIdx.x; t < nbm; t += gridDim.x)
+          for (int j = 0; j < nbn2; ++j)
+            for (int kc = 0; kc < nk2; ++kc, rw.next()) {
+              mbar_wait(w2empty + rw.i, rw.ph ^ 1);
+              mbar_arrive_expect_tx(w2full + rw.i, BN2 * 128);
+              tma_load_2d(w2buf + rw.i * BN2 * 128, &tmb2, w2full + rw.i, kc * KC, j * BN2);
+            }
+      }
+    }
+  } else if (warp == 17) {
     if (lane == 0) {
       const uint32_t idesc1 = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, BN1);
       const uint32_t idesc2 = make_idesc(TcKind<DT>::cf, TcKind<DT>::ab, 128, BN2);
-      Ring rs(stages), rw(2);
-      uint32_t ph_t = 0, ph_a2 = 0;
+      Ring rs(stages), rw(w2slots), ra(2);
+      uint32_t ph_t = 0;
       for (int t = blockIdx.x; t < nbm; t += gridDim.x) {
         // GEMM1: acc1 = X . W1^T over the C_in chunks (acc1 was drained: tready of the last tile)
         for (int kc = 0; kc < nk1; ++kc, rs.next()) {
@@ -1483,31 +1499,31 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(tready, ph_t);
         ph_t ^= 1;
         tc_fence_after();
-        for (int j = 0; j < nbn2; ++j) {
-          mbar_wait(acc2empty, ph_a2 ^ 1);
+        for (int j = 0; j < nbn2; ++j, ra.next()) {
+          mbar_wait(acc2empty + ra.i, ra.ph ^ 1);
           tc_fence_after();
+          const uint32_t d2 = tacc2 + ra.i * BN2;
           for (int kc = 0; kc < nk2; ++kc, rw.next()) {
-            mbar_wait(w2full + rw.i, rw.ph);
+            const int sl = resW2 ? j * nk2 + kc : rw.i;
+            mbar_wait(w2full + sl, resW2 ? 0 : rw.ph);
             tc_fence_after();
             const uint64_t ad = smem_desc_sw128(smem_u32(tbuf + kc * 16384));
-            const uint64_t bd = smem_desc_sw128(smem_u32(w2buf + rw.i * BN2 * 128));
+            const uint64_t bd = smem_desc_sw128(smem_u32(w2buf + sl * BN2 * 128));
             const int ksteps = min(4, (Cmid - kc * KC + KSTEP - 1) / KSTEP);
             for (int k = 0; k < ksteps && !(dbg & 256); ++k)
-              mma_ss<KIND>(tacc2, ad + 2 * k, bd + 2 * k, idesc2, (kc | k) != 0);
-            mma_commit(w2empty + rw.i);
+              mma_ss<KIND>(d2, ad + 2 * k, bd + 2 * k, idesc2, (kc | k) != 0);
+            if (!resW2) mma_commit(w2empty + rw.i);
           }
-          mma_commit(acc2full);
-          ph_a2 ^= 1;
+          mma_commit(acc2full + ra.i);
         }
         mma_commit(tfree);  // every GEMM2 of this tile has read T
       }
     }
-  } else {
-    // epilogue warps 0-3: lane quadrant q = warp (32 rows each)
+  } else if (warp < 4) {
+    // epilogue 1, warps 0-3 (lane quadrant q = warp): acc1 -> eps1 -> T (SW128 K-major, FM dtype)
     const int q = warp;
     const int m = q * 32 + lane;
-    uint32_t ph_a1 = 0, ph_f = 0, ph_a2 = 0;
-    int sbuf = 0;
+    uint32_t ph_a1 = 0, ph_f = 0;
     bool first = true;
     for (int t = blockIdx.x; t < nbm; t += gridDim.x) {
       mbar_wait_sleep(acc1full, ph_a1);
@@ -1518,8 +1534,6 @@ __global__ void __launch_bounds__(192, 1)
       }
       first = false;
       tc_fence_after();
-      // T = eps1(acc1) in the FM dtype, written as SW128 K-major rows (zero columns past C_mid are
-      // matched by TMA zero fill in W2)
       for (int c0 = 0; c0 < nk2 * KC; c0 += 16) {
         uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // columns past the GEMM1 width: zeros (never stale TMEM)
         if (c0 < BN1) {
@@ -1537,22 +1551,27 @@ __global__ void __launch_bounds__(192, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(tready);
-      for (int j = 0; j < nbn2; ++j) {
-        mbar_wait_sleep(acc2full, ph_a2);
-        ph_a2 ^= 1;
+    }
+  } else if (warp < 16) {
+    // epilogue 2, warps 4-15: three warps per lane quadrant split a slice's 128-byte column chunks
+    const int w2i = warp - 4, hs = w2i >> 2;
+    Ring ra(2);
+    int sbuf = 0;
+    for (int t = blockIdx.x; t < nbm; t += gridDim.x) {
+      for (int j = 0; j < nbn2; ++j, ra.next()) {
+        mbar_wait_sleep(acc2full + ra.i, ra.ph);
         tc_fence_after();
-        const int n0 = j * BN2;
-        epilogue_tile_warp<DT>(tacc2, BN2, n0, N, cs2, ep2, stage + warp * 4096, sbuf, 0, 1,
+        epilogue_tile_warp<DT>(tacc2 + ra.i * BN2, BN2, j * BN2, N, cs2, ep2, stage + w2i * 4096, sbuf, hs, 3,
                                [&](const uint8_t* buf, int c, int rr) { tma_store_2d(&tmy, buf, c, t * 128 + rr); });
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(acc2empty);
+        if (lane == 0) mbar_arrive(acc2empty + ra.i);
       }
     }
     if (lane == 0) bulk_wait_all();
   }
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 17) {
     tc_fence_after();
     tmem_dealloc_rt(tbase, tmem_cols);
   }
@@ -1565,7 +1584,7 @@ static int launch_pwpw_t(const void* x, const void* w1, const Epi& ep1, const vo
   constexpr int KC = 128 / ES;
   if (Cmid > 128) return set_error(FCM_E_UNSUPPORTED, "pwpw: C_mid > 128 (T must fit one M=128 x N<=128 accumulator)");
   const int BN1 = round_up(Cmid, 16);
-  int nbn2 = (N + 255) / 256;
+  int nbn2 = (N + 191) / 192;  // BN2 <= 192: acc1 (128) + 2 x BN2 TMEM columns <= 512
   int BN2 = round_up((N + nbn2 - 1) / nbn2, 16);
   nbn2 = (N + BN2 - 1) / BN2;
   CUtensorMap ta, tb1, tb2, ty;
@@ -1594,7 +1613,12 @@ static int launch_pwpw_t(const void* x, const void* w1, const Epi& ep1, const vo
   const int nk2 = (Cmid + KC - 1) / KC;
   const int ncap1 = round_up(nk2 * KC, 16), ncap2 = round_up(nbn2 * BN2, 16);
   const int sA = 16384 + BN1 * 128;
-  const int fixed = 1024 + nk2 * 16384 + 2 * BN2 * 128 + 4 * 4096 + consts_bytes<DT>(ncap1) + consts_bytes<DT>(ncap2) + 512;
+  // W2 resident (all nbn2 x nk2 chunks loaded once per CTA) when that still leaves >= 3 stages
+  const int base = 1024 + nk2 * 16384 + 12 * 4096 + consts_bytes<DT>(ncap1) + consts_bytes<DT>(ncap2) + 1024;
+  const int nres = nbn2 * nk2;
+  const bool resW2 = nres <= 24 && base + nres * BN2 * 128 + 3 * sA <= device_props().smem_optin;
+  const int w2slots = resW2 ? nres : 2;
+  const int fixed = base + w2slots * BN2 * 128;
   const int stages = std::min(6, (device_props().smem_optin - fixed) / sA);
   if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pwpw: not enough shared memory for 2 stages");
   const size_t smem = (size_t)fixed + (size_t)stages * sA;
@@ -1602,8 +1626,8 @@ static int launch_pwpw_t(const void* x, const void* w1, const Epi& ep1, const vo
   const int grid = std::min(nbm, device_props().sms);
   auto kern = pwpw_tc_kernel<DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_k(kern, dim3(grid), dim3(192), smem, st, ta, tb1, tb2, ty, ep1, ep2, M, K1, Cmid, N, BN1, BN2, nbn2, stages,
-           pow2_cols(128 + BN2), ncap1, ncap2, debug_flags());
+  launch_k(kern, dim3(grid), dim3(608), smem, st, ta, tb1, tb2, ty, ep1, ep2, M, K1, Cmid, N, BN1, BN2, nbn2, stages,
+           w2slots, resW2 ? 1 : 0, pow2_cols(128 + 2 * BN2), ncap1, ncap2, debug_flags());
   return check_launch("pwpw_tc_kernel");
 }
 
