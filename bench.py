@@ -97,7 +97,8 @@ def dist_env():
 
 
 def kernel_family(op):
-    return {"dw": "dw_nhwc_kernel", "pw": "pw_tc_kernel", "dwpw": "dwpw_tc_kernel", "pwdw_r": "pwdw_tc_kernel"}[op]
+    return {"dw": "dw_nhwc_kernel", "pw": "pw_tc_kernel", "dwpw": "dwpw_tc_kernel", "pwdw_r": "pwdw_tc_kernel",
+            "pwpw": "pwpw_tc_kernel"}[op]
 
 
 def per_entry_times(netw, reps=20):

@@ -76,12 +76,32 @@ def dwpw_tile_alternatives(tile, ho, wo, k, s, cout, dtype, limit=10):
     return [uniq[0]] + rest[:limit - 1]
 
 
+def pwpw_candidates(model: dict, probe, dtype: str, batch: int):
+    """FCM PWPW candidates: every producer -> consumer edge between two PW
+    layers, with the §8(d)-style compulsory bytes (T never reaches HBM: 2 b |T| saved)."""
+    esize = {"f32": 4, "bf16": 2, "f16": 2, "s8": 1}[dtype]
+    kinds = {l["id"]: l for l in model["layers"]}
+    out = []
+    for a, b in model["edges"]:
+        la, lb = kinds[a], kinds[b]
+        if la["kind"] != "pw" or lb["kind"] != "pw":
+            continue
+        m = batch * la["h"] * la["w"]
+        cin, cmid, cout = la["c_in"], la["c_out"], lb["c_out"]
+        dram = esize * (m * (cin + cout) + cin * cmid + cmid * cout)
+        out.append({"op": "pwpw", "kind": "pwpw", "layers": [a, b], "tile": None, "dram_bytes": dram, "l2_bytes": dram,
+                    "lbl_dram_bytes": dram + 2 * esize * m * cmid, "pred_us": 0.0,
+                    "macs": m * (cin * cmid + cmid * cout)})
+    return out
+
+
 def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=False, tile_search=True):
     plan = fcm.plan(model_json(net, dtype, batch))
     cands = plan["candidates"]
     # one Network instance whose "plan" is every candidate, so each has real buffers to run on
     all_entries = [dict(c) for c in cands["lbl"]] + [dict(c) for c in cands["fcm"]]
     probe = Network(net, dtype, batch, {"entries": []}, device=device)
+    all_entries += pwpw_candidates(model_json(net, dtype, batch), probe, dtype, batch)
     order = probe.order
     meas = {}
     for c in all_entries:

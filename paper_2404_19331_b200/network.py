@@ -132,6 +132,9 @@ class Network:
             l = self.layers[lids[0]]
             (wd, ed), (wp, ep) = self.params[lids[0]], self.params[lids[1]]
             return lambda: fcm.dwpw(src, wd, l["stride"], None, ed, wp, ep, out=out, tile=tile)
+        if op == "pwpw":
+            (w1, e1), (w2, e2) = self.params[lids[0]], self.params[lids[1]]
+            return lambda: fcm.pwpw(src, w1, e1, w2, e2, out=out)
         if op == "pwdw_r":
             l = self.layers[lids[1]]
             (wp, ep), (wd, ed) = self.params[lids[0]], self.params[lids[1]]

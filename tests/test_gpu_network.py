@@ -60,3 +60,36 @@ def test_pdl_does_not_change_results(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(torch.load(f))
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("net,dt,batch", [("mobilenet_v2", "bf16", 2), ("mobilenet_v1", "s8", 2)])
+def test_stack_with_pwpw_equals_layer_by_layer(net, dt, batch):
+    # replace PW -> PW chain pairs of the all-LBL plan by FCM PWPW entries: identical bytes (the
+    # PWPW kernel rounds / requantises T exactly like the unfused PW epilogue)
+    import paper_2404_19331_b200 as fcm
+    from paper_2404_19331_b200.autotune import pwpw_candidates
+    from paper_2404_19331_b200.network import Network, model_json
+    plan = fcm.plan(model_json(net, dt, batch))
+    lbl = _lbl_plan(plan)
+    probe = Network(net, dt, batch, {"entries": []})
+    cands = {tuple(c["layers"]): c for c in pwpw_candidates(model_json(net, dt, batch), probe, dt, batch)}
+    ents, i, used = [], 0, 0
+    while i < len(lbl["entries"]):
+        e = lbl["entries"][i]
+        if i + 1 < len(lbl["entries"]):
+            key = (e["layers"][0], lbl["entries"][i + 1]["layers"][0])
+            if key in cands and probe.layers[key[0]]["c_out"] <= 128 and probe.layers[key[0]]["c_out"] % 16 == 0:
+                ents.append(cands[key])
+                i += 2
+                used += 1
+                continue
+        ents.append(e)
+        i += 1
+    if used == 0:
+        pytest.skip("no PW -> PW chain pair in this stack")
+    a = Network(net, dt, batch, dict(lbl, entries=ents))
+    a.run()
+    b = Network(net, dt, batch, lbl)
+    b.run()
+    torch.cuda.synchronize()
+    assert torch.equal(a.out.cpu(), b.out.cpu())

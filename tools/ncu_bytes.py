@@ -21,7 +21,7 @@ launch = {}
 for r in rows[1:]:
     name = r[iN].split("<")[0].replace("void ", "").replace("fcm::", "")
     if name not in ("dw_nhwc_kernel", "dw_nchw_kernel", "pw_tc_kernel", "dwpw_tc_kernel", "pwdw_tc_kernel",
-                    "pw_simt_kernel", "dw_nhwc_simt_kernel", "dwpw_simt_kernel", "pwdw_simt_kernel"):
+                    "pw_simt_kernel", "dw_nhwc_simt_kernel", "dwpw_simt_kernel", "pwdw_simt_kernel", "pwpw_tc_kernel"):
         continue
     d = launch.setdefault(int(r[iID]), {"kernel": name})
     d[r[iM]] = float(r[iV].replace(",", "")) * UNIT.get(r[iU], 1)
