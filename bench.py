@@ -27,7 +27,9 @@ sys.path.insert(0, ROOT)
 METRIC = "fused DW+PW layer µs & HBM GB/s vs B200 peak; MobileNetV2 images/sec @1/2/4/8"
 # BASELINE.json configs index of each network's stack (configs[0] is the single-layer parity case)
 CONFIG_OF = {"single_dwpw": "configs[0]", "mobilenet_v1": "configs[1]", "mobilenet_v2": "configs[2]",
-             "efficientnet_b0": "configs[3]", "cvt13": "configs[4]"}
+             "efficientnet_b0": "configs[3]", "cvt13": "configs[4]",
+             "xception": "SURVEY 8(f) rank 2, 299x299", "ceit_leff": "SURVEY 8(f) rank 2",
+             "cmt_irffn": "SURVEY 8(f) rank 2"}
 DTYPE_NAME = {"bf16": "bf16", "f16": "f16", "s8": "s8", "f32": "f32"}
 
 
@@ -88,6 +90,31 @@ class Clocks:
                 "samples": len(sm)}
 
 
+# ------------------------------------------------------------------------------ energy
+def energy_per_image(replay, images_per_replay, ms_per_replay, gpu_index, seconds=2.0):
+    """Energy per inference, the analogue of the paper's energy experiment: NVML's
+    cumulative board energy counter (mJ) read around >= `seconds` of back-to-back replays of the
+    captured step. Board energy includes idle/static power, as a wall-socket meter would."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        n = max(1, int(seconds * 1e3 / max(ms_per_replay, 1e-3)))
+        torch.cuda.synchronize()
+        t0, e0 = time.perf_counter(), pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+        for _ in range(n):
+            replay()
+        torch.cuda.synchronize()
+        t1, e1 = time.perf_counter(), pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+        pynvml.nvmlShutdown()
+        joules = (e1 - e0) / 1e3
+        return {"j_per_image": round(joules / (n * images_per_replay), 6), "avg_power_w": round(joules / (t1 - t0), 1),
+                "seconds": round(t1 - t0, 3), "images": n * images_per_replay,
+                "method": "NVML total energy counter around back-to-back graph replays (board power)"}
+    except Exception as e:  # reporting only; never fails the bench
+        return {"error": str(e)[:200]}
+
+
 # ------------------------------------------------------------------------------ helpers
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -139,7 +166,7 @@ def cpu_baseline(net, dtype, seconds=15.0):
             "sample": f"{n} images x whole {net} DW/PW stack ({dtype}), one at a time, {dt:.1f}s"}
 
 
-def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5):
+def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5, energy_gpu=None):
     """cuDNN's unfused DW + PW (PyTorch F.conv2d, channels_last, cudnn.benchmark) on the same layers
     and synthetic weights: BN scale folded into the weights, bias in the conv, activation as an
     in-place clamp. Captured in a CUDA graph; device time per step via CUDA events."""
@@ -168,12 +195,13 @@ def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5):
     def run():
         y = x
         for kind, w, b, l in layers:
+            cin = l["c"] if kind == "dw" else l["c_in"]
+            if tuple(y.shape[1:]) != (cin, l["h"], l["w"]):  # a stage token map / pooled map input
+                y = torch.zeros(batch, cin, l["h"], l["w"], device=dev, dtype=tdt).contiguous(
+                    memory_format=torch.channels_last)
             if kind == "dw":
                 y = F.conv2d(y, w, b, stride=l["stride"], padding=l["k"] // 2, groups=l["c"])
             else:
-                if y.shape[1] != w.shape[1]:  # CvT: every projection block reads a stage token map
-                    y = torch.zeros(batch, w.shape[1], l["h"], l["w"], device=dev, dtype=tdt).contiguous(
-                        memory_format=torch.channels_last)
                 y = F.conv2d(y, w, b)
             if l["act"] == 2:
                 y.clamp_(0, 6)
@@ -198,8 +226,11 @@ def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    return {"value": round(batch / (ms / 1e3), 1), "unit": "images/s", "ms_per_step": round(ms, 4),
-            "kind": "torch F.conv2d (cuDNN), unfused DW + PW, folded BN, channels_last, CUDA graph"}
+    out = {"value": round(batch / (ms / 1e3), 1), "unit": "images/s", "ms_per_step": round(ms, 4),
+           "kind": "torch F.conv2d (cuDNN), unfused DW + PW, folded BN, channels_last, CUDA graph"}
+    if energy_gpu is not None:
+        out["energy"] = energy_per_image(g.replay, batch, ms, energy_gpu)
+    return out
 
 
 def traffic_from_profiles(kernel, config_tag):
@@ -239,7 +270,7 @@ def run_reference(args, ws, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic", "config": {"workload": f"{args.net} DW/PW stack "
                                                         f"({CONFIG_OF.get(args.net, 'not a BASELINE config')}), "
-                                                        f"{args.batch} img/GPU, 224x224",
+                                                        f"{args.batch} img/GPU",
                                             "net": args.net, "global_batch": ws * args.batch,
                                             "images_per_step": per_step,
                                             "sample": "the oracle processes a bounded sample of the batch per step"},
@@ -279,6 +310,7 @@ def main():
     ap.add_argument("--no-cudnn", action="store_true", help="skip the cuDNN unfused DW+PW baseline")
     ap.add_argument("--layers-out", default="", help="write the per-entry table (JSON) here")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly (for ncu launch lists)")
+    ap.add_argument("--no-energy", action="store_true", help="skip the NVML energy-per-image measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -345,6 +377,9 @@ def main():
     barrier()
     t_ms = e0.elapsed_time(e1)
     clk = clocks.stop()
+    energy = None
+    if not args.no_energy and not args.no_graph:
+        energy = energy_per_image(graph.replay, args.batch, t_ms / args.steps, local)
 
     # ---------------- end-to-end through the public API with host buffers
     # Every step copies its batch host->device (pinned) and its output device->host inside the
@@ -447,7 +482,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded splitmix64 inputs/weights, random-init)",
             "config": {"workload": f"{args.net} DW/PW stack ({CONFIG_OF.get(args.net, 'not a BASELINE config')}), "
-                                   f"{args.batch} img/GPU, 224x224",
+                                   f"{args.batch} img/GPU",
                        "net": args.net, "global_batch": ws * args.batch, "plan_mode": plan["mode"],
                        "fused_pairs": plan["totals"]["fused_pairs"], "kernels_per_step": launches_per_step,
                        "parallelism": f"batch-sharded x{ws} (replicas, no collective on the hot path)",
@@ -468,13 +503,19 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
         }
+        if energy is not None:
+            line["energy"] = energy
         if ws > 1:
             line["verify"] = verify
         if not args.no_cudnn and args.dtype in ("bf16", "f16", "f32"):
             try:
-                cb = cudnn_stack(args.net, args.dtype, args.batch, dev)
+                cb = cudnn_stack(args.net, args.dtype, args.batch, dev,
+                                 energy_gpu=None if (args.no_energy or energy is None) else local)
                 if cb:
                     cb["fcm_speedup"] = round(line["value"] / ws / cb["value"], 3)
+                    ce, fe = cb.get("energy", {}), line.get("energy", {})
+                    if "j_per_image" in ce and "j_per_image" in fe and fe["j_per_image"] > 0:
+                        cb["fcm_energy_ratio"] = round(fe["j_per_image"] / ce["j_per_image"], 3)
                     line["cudnn_baseline"] = cb
             except Exception as e:  # baseline only; never fails the bench
                 line["cudnn_baseline"] = {"error": str(e)[:200]}

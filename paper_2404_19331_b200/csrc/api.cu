@@ -208,7 +208,7 @@ int fcm_dw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const
   if (x->layout == FCM_NCHW) return launch_dw_nchw(x->dtype, x->data, w_dw, to_epi(ep), y->data, g, st);
   // channel pitch not a multiple of 16 B: TMA cannot address it -> CUDA-core kernel
   if (!pitch_ok(x)) return launch_dw_simt(x->dtype, x->data, w_dw, to_epi(ep), y->data, g, st);
-  default_dw_tile(g);
+  default_dw_tile(g, elem_size(x->dtype));
   if (tile) {
     if (tile->tile_h > 0) g.th = tile->tile_h;
     if (tile->tile_w > 0) g.tw = tile->tile_w;

@@ -557,6 +557,90 @@ __device__ __forceinline__ uint32_t pack_act(uint64_t acc, uint32_t hi2) {
   return h;
 }
 
+// ---------------------------------------------------------------------------- int8 column-pair FFMA2 DW core
+// int8, 3x3. Exact in fp32: every product |x w| <= 128 * 127 and every partial sum (9 taps + the
+// int32 bias, |acc| < 9 * 128 * 128 + 2^12 < 2^22) is an integer below 2^24, so FFMA2 accumulation
+// is bit-exact whatever the order (SURVEY §8(c) "Exactness bound for fp32-accumulated int8 DW").
+// A lane owns one 32-bit word (4 channels) of two adjacent output columns: per input word one
+// XOR + 4 byte permutes build 2^23 + (x + 128) as fp32 bit patterns, one FFMA2 pair subtracts
+// 2^23 + 128 (exact), and the channel pairs (0,1), (2,3) feed packed FFMA2s.
+__device__ __forceinline__ void i8word_to_f2x2(uint32_t w, uint64_t& lo, uint64_t& hi) {
+  const uint32_t u = w ^ 0x80808080u;
+  uint32_t b0, b1, b2, b3;
+  asm("prmt.b32 %0, %1, 0x4B000000, 0x7440;" : "=r"(b0) : "r"(u));
+  asm("prmt.b32 %0, %1, 0x4B000000, 0x7441;" : "=r"(b1) : "r"(u));
+  asm("prmt.b32 %0, %1, 0x4B000000, 0x7442;" : "=r"(b2) : "r"(u));
+  asm("prmt.b32 %0, %1, 0x4B000000, 0x7443;" : "=r"(b3) : "r"(u));
+  const uint64_t one2 = f2_pack(1.f, 1.f), nb2 = f2_pack(-8388736.f, -8388736.f);
+  lo = f2_fma(f2_pack(__uint_as_float(b0), __uint_as_float(b1)), one2, nb2);
+  hi = f2_fma(f2_pack(__uint_as_float(b2), __uint_as_float(b3)), one2, nb2);
+}
+
+template <int S, int SEG, class Sink>
+__device__ __forceinline__ void dw3_pair_i8(uint32_t src, int col_bytes, int row_bytes, int y0, int max_row,
+                                            const uint64_t (&W)[9][2], const uint64_t (&bias)[2], Sink&& sink) {
+  constexpr int NCW = 3 + S;
+  constexpr int WR = (SEG - 1) * S + 3;
+  constexpr int PD = 2;
+  uint64_t acc[SEG][2][2];
+  uint32_t raw[WR][NCW];
+  auto load_row = [&](int ii) {
+    const uint32_t rp = src + min(y0 * S + ii, max_row) * row_bytes;
+#pragma unroll
+    for (int j = 0; j < NCW; ++j) raw[ii][j] = lds32(rp + j * col_bytes);
+  };
+#pragma unroll
+  for (int ii = 0; ii < PD && ii < WR; ++ii) load_row(ii);
+#pragma unroll
+  for (int ii = 0; ii < WR; ++ii) {
+    if (ii + PD < WR) load_row(ii + PD);
+    uint64_t x[NCW][2];
+#pragma unroll
+    for (int j = 0; j < NCW; ++j) i8word_to_f2x2(raw[ii][j], x[j][0], x[j][1]);
+#pragma unroll
+    for (int r = 0; r < SEG; ++r) {
+      const int i = ii - r * S;
+      if (i < 0 || i > 2) continue;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            acc[r][c][h] = f2_fma(x[c * S + j][h], W[i * 3 + j][h], (i == 0 && j == 0) ? bias[h] : acc[r][c][h]);
+      if (i == 2) sink(r, acc[r]);
+    }
+  }
+}
+
+// Per-channel int8 requantiser in the form the FFMA2 core's epilogue uses. For sh >= 33 the
+// rounding term 2^(sh-1) has no low-word bits, so (acc M + 2^(sh-1)) >> sh ==
+// (mulhi(acc, M) + 2^(sh-33)) >> (sh-32) exactly (floor((n + f) / 2^k) = floor(n / 2^k) for integer
+// n, 0 <= f < 1): one mad.hi + one shift. Smaller shifts take the 64-bit form.
+struct RqI8 {
+  int32_t m, c, s;  // multiplier, addend, shift (fast form: c = 2^(sh-33), s = sh - 32; else c = -1, s = sh)
+};
+__device__ __forceinline__ RqI8 make_rq(int32_t m, int32_t sh) {
+  return sh >= 33 ? RqI8{m, 1 << (sh - 33), sh - 32} : RqI8{m, -1, sh};
+}
+__device__ __forceinline__ int32_t rq_apply(int32_t a, const RqI8& q) {
+  if (q.c >= 0) {
+    int32_t h;
+    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(a), "r"(q.m), "r"(q.c));
+    return h >> q.s;
+  }
+  const long long p = static_cast<long long>(a) * q.m + (1LL << (q.s - 1));
+  return static_cast<int32_t>(p >> q.s);
+}
+// fp32 pair holding exact integers |v| < 2^22 -> int32 pair (magic-number rounding: the bits of
+// v + 1.5 * 2^23 are 0x4B400000 + v).
+__device__ __forceinline__ void f2_to_i2(uint64_t v, int32_t& a, int32_t& b) {
+  float x, y;
+  f2_unpack(f2_fma(v, f2_pack(1.f, 1.f), f2_pack(12582912.f, 12582912.f)), x, y);
+  a = static_cast<int32_t>(__float_as_uint(x) - 0x4B400000u);
+  b = static_cast<int32_t>(__float_as_uint(y) - 0x4B400000u);
+}
+
 // Stage the 3x3 DW weights of C channels as scale-folded fp32 pairs [9][cwords] (uint64) plus the
 // bias pairs [cwords], zero past C. Both arrays are read back with ld.shared.u64 per lane.
 template <int DT>

@@ -16,7 +16,7 @@ template <int DT, int K, int S>
 __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CUtensorMap tmx,
                                                       const typename Tr<DT>::T* __restrict__ wdw, Epi ep,
                                                       typename Tr<DT>::T* __restrict__ y, int C, int Ho, int Wo,
-                                                      int pt, int pl, int th, int tw, int tiles_x, int tiles_y) {
+                                                      int pt, int pl, int th, int tw, int tiles_x, int tiles_y, int pb) {
   pdl_launch();
   pdl_wait();
   constexpr int V = Tr<DT>::VEC;
@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
   const int n = t / tiles_y;
   const int c0 = blockIdx.y * KC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pwd = pb >> 2;  // staged 32-bit words per pixel (128 B, or C * ES when C is narrower)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmx);
     mbar_init(&bar, 1);
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar, th_in * tw_in * 128);
+    mbar_arrive_expect_tx(&bar, th_in * tw_in * pb);
     tma_load_4d(xs, &tmx, &bar, c0, tx * tw * S - pl, ty * th * S - pt, n);
   }
   const int y0 = ty * th, x0 = tx * tw;
@@ -68,12 +69,79 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
       const int x = x0 + col;
       const bool live = col < tw && x < Wo && cval;
       const int ys = seg * kSeg;
-      const uint32_t src = smem_u32(xs) + (((live ? col : 0) * S) * 32 + wd) * 4;
+      const uint32_t src = smem_u32(xs) + (((live ? col : 0) * S) * pwd + wd) * 4;
       uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + (live ? x : 0)) * C + cl) / V;
       const size_t rstride = (size_t)Wo * C / V;
       const int nvalid = live ? nrows - ys : 0;
-      dw_segh<DT, K, S, kSeg>(src, 128, tw_in * 128, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
+      dw_segh<DT, K, S, kSeg>(src, pb, tw_in * pb, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
         if (r < nvalid) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
+      });
+    }
+    return;
+  } else if constexpr (DT == FCM_S8 && K == 3) {
+    // int8 column-pair FFMA2 core (exact, see dw3_pair_i8); a lane owns one word (4 channels) of
+    // two adjacent output columns; lane groups for partly filled 128-channel groups as above
+#ifndef FCM_I8SEG
+#define FCM_I8SEG 8
+#endif
+    constexpr int kSeg = (S == 1) ? FCM_I8SEG : 4;
+    const int cw_valid = min(32, (C - c0) / 4);
+    const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+    const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+    const int cl = c0 + wd * 4;
+    const bool cval = wd < cw_valid;
+    uint64_t W[9][2], bias[2];
+    RqI8 rq[4];
+    {
+      const uint32_t* g = reinterpret_cast<const uint32_t*>(wdw);
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const uint32_t w = cval ? __ldg(g + t * (C / 4) + cl / 4) : 0u;
+        float f[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) f[v] = static_cast<float>(static_cast<int32_t>(w << (24 - 8 * v)) >> 24);
+        W[t][0] = f2_pack(f[0], f[1]);
+        W[t][1] = f2_pack(f[2], f[3]);
+      }
+      float b[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        b[v] = (cval && ep.bias_q) ? static_cast<float>(__ldg(ep.bias_q + cl + v)) : 0.f;
+        rq[v] = make_rq(cval ? __ldg(ep.mult_q + cl + v) : 0, cval ? __ldg(ep.shift_q + cl + v) : 40);
+      }
+      bias[0] = f2_pack(b[0], b[1]);
+      bias[1] = f2_pack(b[2], b[3]);
+    }
+    const int zp = ep.zp_out, qmin = ep.qmin, qmax = ep.qmax;
+    mbar_wait(&bar, 0);
+    const int nseg = (nrows + kSeg - 1) / kSeg;
+    const int ncolp = (tw + 1) / 2;
+    const int ncolg = (ncolp + npix - 1) / npix;
+    const size_t rstride = (size_t)Wo * C / 4;
+    for (int item = warp; item < ncolg * nseg; item += 4) {
+      const int cg = item / nseg, seg = item - cg * nseg;
+      const int cp = cg * npix + grp;
+      const int col = 2 * cp, x = x0 + col;
+      const bool live0 = cp < ncolp && x < Wo && cval;
+      const bool live1 = live0 && col + 1 < tw && x + 1 < Wo;
+      const int ys = seg * kSeg;
+      const uint32_t src = smem_u32(xs) + (((live0 ? col : 0) * S) * pwd + wd) * 4;
+      uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + (live0 ? x : 0)) * C + cl) / 4;
+      const int nvalid = live0 ? nrows - ys : 0;
+      dw3_pair_i8<S, kSeg>(src, pb, tw_in * pb, ys, th_in - 1, W, bias, [&](int r, const uint64_t (&a)[2][2]) {
+        if (r < nvalid) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            int32_t v[4];
+            f2_to_i2(a[c][0], v[0], v[1]);
+            f2_to_i2(a[c][1], v[2], v[3]);
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              word |= (static_cast<uint32_t>(min(max(rq_apply(v[q], rq[q]) + zp, qmin), qmax)) & 0xFFu) << (8 * q);
+            if (c == 0 || live1) dst[r * rstride + c * (C / 4)] = word;
+          }
+        }
       });
     }
     return;
@@ -94,8 +162,8 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
       const int col = cb + grp;
       const int x = x0 + col;
       const bool live = col < tw && x < Wo;
-      const uint32_t src = smem_u32(xs) + (((live ? col : cb) * S) * 32 + wd) * 4;
-      dw_segment<DT, K, S>(src, 128, tw_in * 128, 0, nrows, th_in - 1, W,
+      const uint32_t src = smem_u32(xs) + (((live ? col : cb) * S) * pwd + wd) * 4;
+      dw_segment<DT, K, S>(src, pb, tw_in * pb, 0, nrows, th_in - 1, W,
                            [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
                              if (live && cl < C) {
                                const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
@@ -176,18 +244,23 @@ static int launch_dw_t(const void* x, const void* wdw, const Epi& ep, void* y, c
   CUtensorMap tm;
   const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
   const uint64_t strides[3] = {(uint64_t)g.C * ES, (uint64_t)g.W * g.C * ES, (uint64_t)g.H * g.W * g.C * ES};
-  const uint32_t box[4] = {(uint32_t)KC, (uint32_t)tw_in, (uint32_t)th_in, 1};
+  // channel box: one 128-byte group, or the whole (16-byte multiple) pixel when C is narrower --
+  // no out-of-bounds fill traffic and 4x less shared memory for e.g. int8 C = 32
+  const int pb = (g.C * ES < 128) ? g.C * ES : 128;
+  const uint32_t box[4] = {(uint32_t)(pb / ES), (uint32_t)tw_in, (uint32_t)th_in, 1};
   if (!encode_tmap(&tm, tmap_dtype(DT), 4, x, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
     return set_error(FCM_E_CUDA, "cuTensorMapEncodeTiled failed for the DW input");
   const int tiles_x = (g.Wo + tw - 1) / tw, tiles_y = (g.Ho + th - 1) / th;
-  const size_t smem = (size_t)th_in * tw_in * 128;
+  // + 2 columns of slack: the int8 column-pair core reads S extra input words past the last
+  // column of an odd-width tile (its second output column is dead, never stored)
+  const size_t smem = (size_t)th_in * tw_in * pb + 256;
   if (smem > (size_t)device_props().smem_optin) return set_error(FCM_E_INFEASIBLE, "dw tile exceeds shared memory");
   auto kern = dw_nhwc_kernel<DT, K, S>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(tiles_x * tiles_y * g.N, (g.C + KC - 1) / KC);
   using TT = typename Tr<DT>::T;
   launch_k(kern, dim3(grid), dim3(128), smem, st, tm, static_cast<const TT*>(wdw), ep, static_cast<TT*>(y), g.C, g.Ho, g.Wo, g.pt, g.pl,
-                                th, tw, tiles_x, tiles_y);
+                                th, tw, tiles_x, tiles_y, pb);
   return check_launch("dw_nhwc_kernel");
 }
 

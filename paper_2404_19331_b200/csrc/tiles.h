@@ -21,9 +21,14 @@ inline int pick_bn(int N, int nsplit, int cpc, int& nb_out) {
 }
 
 // LBL DW: one 128-byte channel group x th x tw outputs per CTA.
-inline void default_dw_tile(Geo& g) {
-  g.th = std::min(g.s == 1 ? 8 : 4, g.Ho);
-  g.tw = std::min(16, g.Wo);
+inline void default_dw_tile(Geo& g, int es = 0) {
+  // 8 x 16 (s1) / 4 x 16 (s2) output pixels of one 128-byte channel group; a narrower pixel
+  // (C * es < 128 B, staged at its own width) gets proportionally more pixels per CTA
+  const int pb = es > 0 ? std::min(128, g.C * es) : 128;
+  const int f = std::max(1, 128 / std::max(pb, 1));
+  const int fh = f >= 4 ? 2 : 1, fw = f / fh >= 2 ? 2 : 1;
+  g.th = std::min((g.s == 1 ? 8 : 4) * fh, g.Ho);
+  g.tw = std::min(16 * fw, g.Wo);
   g.nb = 1;
 }
 

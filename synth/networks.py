@@ -11,7 +11,7 @@ Stem convolutions, SE, pooling and classifier heads are not DW/PW layers and are
 """
 from __future__ import annotations
 
-from synth import ACT_NONE, ACT_RELU6
+from synth import ACT_NONE, ACT_RELU, ACT_RELU6
 
 
 def _dw(h, w, c, k, s, act=ACT_RELU6):
@@ -87,13 +87,51 @@ def cvt13_projections():
     return blocks
 
 
+def xception():
+    """the separable convolutions of Xception at 299x299
+    (entry flow after the two stem convs, 8x3 middle flow, exit flow). A separable conv is
+    DW 3x3 (no BN/activation in between) -> PW, BN, ReLU. Max-pools between entry/exit blocks and
+    the 1x1 s2 residual shortcuts are not DW/PW layers (omitted); a block after a pool reads a
+    fresh map of the pooled size."""
+    spec = [(147, 64, 128), (147, 128, 128), (74, 128, 256), (74, 256, 256), (37, 256, 728), (37, 728, 728)]
+    spec += [(19, 728, 728)] * 24 + [(19, 728, 728), (19, 728, 1024), (10, 1024, 1536), (10, 1536, 2048)]
+    return [[_dw(hw, hw, ci, 3, 1, ACT_NONE), _pw(hw, hw, ci, co, ACT_RELU)] for hw, ci, co in spec]
+
+
+def ceit_leff():
+    """the LeFF modules of CeiT-T (12 blocks on the 14x14
+    token map, C = 192, expansion 4): PW 192->768, DW 3x3, PW 768->192. GELU is read as ReLU
+    (GELU is §8(f) rank 4); attention sits between blocks, so each LeFF reads the stage map."""
+    return [[_pw(14, 14, 192, 768, ACT_RELU), _dw(14, 14, 768, 3, 1, ACT_RELU), _pw(14, 14, 768, 192, ACT_RELU)]
+            for _ in range(12)]
+
+
+def cmt_irffn():
+    """the IRFFN modules of CMT-S (stages 56/28/14/7 with
+    C = 64/128/256/512 and 3/3/16/3 blocks, expansion 4): PW C->4C, DW 3x3, PW 4C->C. GELU read
+    as ReLU; the DW's residual add is omitted (rank 4); each IRFFN reads its stage map."""
+    blocks = []
+    for hw, c, n in [(56, 64, 3), (28, 128, 3), (14, 256, 16), (7, 512, 3)]:
+        for _ in range(n):
+            blocks.append([_pw(hw, hw, c, 4 * c, ACT_RELU), _dw(hw, hw, 4 * c, 3, 1, ACT_RELU),
+                           _pw(hw, hw, 4 * c, c, ACT_NONE)])
+    return blocks
+
+
 NETWORKS = {
     "single_dwpw": single_dwpw,
     "mobilenet_v1": mobilenet_v1,
     "mobilenet_v2": mobilenet_v2,
     "efficientnet_b0": efficientnet_b0,
     "cvt13": cvt13_projections,
+    "xception": xception,
+    "ceit_leff": ceit_leff,
+    "cmt_irffn": cmt_irffn,
 }
+
+# networks whose DW/PW blocks are separated by non-DW/PW layers (attention): every block reads
+# the stage's token map instead of the previous block's output
+_STAGE_FED = {"cvt13", "ceit_leff", "cmt_irffn"}
 
 
 def layer_ids(blocks):
@@ -127,7 +165,18 @@ def network_params(seed: int, net: str, dtype: str) -> dict:
 def block_source(net: str, blocks, bi: int):
     """Where block bi reads its input: ('chain', None) = previous block's output, or
     ('stage', role) = a stage token map shared by all CvT projections of that stage."""
-    if net != "cvt13":
-        return ("chain", None)
     l = blocks[bi][0]
-    return ("stage", f"{net}/stage_{l['h']}x{l['c']}")
+    c = l["c"] if l["kind"] == "dw" else l["c_in"]
+    if net in _STAGE_FED:
+        return ("stage", f"{net}/stage_{l['h']}x{c}")
+    if bi == 0:
+        return ("chain", None)
+    p = blocks[bi - 1][-1]
+    if p["kind"] == "dw":
+        ph = (p["h"] + 2 * (p["k"] // 2) - p["k"]) // p["stride"] + 1
+        pc = p["c"]
+    else:
+        ph, pc = p["h"], p["c_out"]
+    if (ph, pc) == (l["h"], c):
+        return ("chain", None)
+    return ("stage", f"{net}/pooled_b{bi}_{l['h']}x{c}")  # a pool / non-DW/PW layer in between

@@ -12,7 +12,9 @@ from paper_2404_19331_b200.network import model_json
 
 CASES = [("single_dwpw", "f32", 1), ("single_dwpw", "s8", 1), ("mobilenet_v1", "s8", 64), ("mobilenet_v1", "bf16", 1),
          ("mobilenet_v2", "bf16", 256), ("mobilenet_v2", "bf16", 1), ("efficientnet_b0", "s8", 256),
-         ("efficientnet_b0", "s8", 32), ("cvt13", "bf16", 512)]
+         ("efficientnet_b0", "s8", 32), ("cvt13", "bf16", 512),
+         ("xception", "bf16", 64), ("xception", "s8", 1), ("ceit_leff", "bf16", 256), ("cmt_irffn", "s8", 64),
+         ("cmt_irffn", "bf16", 1)]
 
 
 @pytest.fixture(scope="module")
