@@ -76,6 +76,23 @@ def dwpw_tile_alternatives(tile, ho, wo, k, s, cout, dtype, limit=10):
     return [uniq[0]] + rest[:limit - 1]
 
 
+def dw_tile_alternatives(tile, ho, wo, k, s, c, dtype):
+    """LBL DW output tiles besides the planner's default: small tiles give more CTAs (latency
+    hiding on small maps), large ones less halo; the measurement picks."""
+    esize = {"f32": 4, "bf16": 2, "f16": 2, "s8": 1}[dtype]
+    pb = min(128, c * esize)
+    out, seen = [dict(tile)], {(tile["tile_h"], tile["tile_w"])}
+    for th, tw in [(4, 7), (4, 8), (4, 16), (7, 7), (7, 14), (8, 8), (8, 14), (8, 16), (14, 14), (8, 32),
+                   (16, 16), (16, 32), (28, 28)]:
+        th, tw = min(th, ho), min(tw, wo)
+        th_in, tw_in = (th - 1) * s + k, (tw - 1) * s + k
+        if (th, tw) in seen or th_in > 256 or tw_in > 256 or th_in * tw_in * pb > 110 * 1024:
+            continue
+        seen.add((th, tw))
+        out.append(dict(tile, tile_h=th, tile_w=tw))
+    return out
+
+
 def pwpw_candidates(model: dict, probe, dtype: str, batch: int):
     """FCM PWPW candidates: every producer -> consumer edge between two PW
     layers, with the §8(d)-style compulsory bytes (T never reaches HBM: 2 b |T| saved)."""
@@ -117,6 +134,12 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
             ho = (d["h"] + 2 * (kk // 2) - kk) // ss + 1
             wo = (d["w"] + 2 * (kk // 2) - kk) // ss + 1
             tiles = dwpw_tile_alternatives(c["tile"], ho, wo, kk, ss, probe.layers[lids[1]]["c_out"], dtype)
+        elif tile_search and c["op"] == "dw" and c.get("tile") and c["tile"].get("tile_w", 0) > 1:
+            d = probe.layers[lids[0]]
+            kk, ss = d["k"], d["stride"]
+            ho = (d["h"] + 2 * (kk // 2) - kk) // ss + 1
+            wo = (d["w"] + 2 * (kk // 2) - kk) // ss + 1
+            tiles = dw_tile_alternatives(c["tile"], ho, wo, kk, ss, d["c"], dtype)
         best = None
         for t in tiles:
             ct = dict(c, tile=t) if t is not None else c

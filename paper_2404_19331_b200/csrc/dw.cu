@@ -135,10 +135,21 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
             int32_t v[4];
             f2_to_i2(a[c][0], v[0], v[1]);
             f2_to_i2(a[c][1], v[2], v[3]);
-            uint32_t word = 0;
+            int32_t o[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              word |= (static_cast<uint32_t>(min(max(rq_apply(v[q], rq[q]) + zp, qmin), qmax)) & 0xFFu) << (8 * q);
+            for (int q = 0; q < 4; ++q) o[q] = min(rq_apply(v[q], rq[q]) + zp, qmax);
+            uint32_t word;
+            if (qmin == -128) {  // saturating pack gives the lower clamp
+              asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(word) : "r"(o[3]), "r"(o[2]));
+              asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %0;" : "+r"(word) : "r"(o[1]), "r"(o[0]));
+            } else if (qmin == 0) {  // RELU / RELU6 with zp_out = 0
+              asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(word) : "r"(o[3]), "r"(o[2]));
+              asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %0;" : "+r"(word) : "r"(o[1]), "r"(o[0]));
+            } else {
+              word = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) word |= (static_cast<uint32_t>(max(o[q], qmin)) & 0xFFu) << (8 * q);
+            }
             if (c == 0 || live1) dst[r * rstride + c * (C / 4)] = word;
           }
         }
