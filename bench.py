@@ -454,12 +454,24 @@ def main():
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
     fam = {}
     rows = []
+    # binding roof: per launch max(t_HBM, t_DW on the FFMA pipe, t_PW on the
+    # tensor cores); DW peak = SMs x 128 fp32 MAC/clk x max SM clock (the FFMA/FFMA2 rate,
+    # tools/microbench/fma_rates.cu); PW peak = measured dense bf16 (f16 same, int8 2x, tf32 1/2)
+    sm_hz = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    dw_mac_s = 148 * 128 * sm_hz
+    tc_mac_s = float(pk.get("bf16_tflops", 1598.4)) * 1e12 / 2 * {"s8": 2.0, "f32": 0.5}.get(args.dtype, 1.0)
     for info, us in zip(netw.step_info, times_us):
         k = kernel_family(info["op"])
-        f = fam.setdefault(k, {"us": 0.0, "bytes": 0, "n": 0})
+        f = fam.setdefault(k, {"us": 0.0, "bytes": 0, "n": 0, "bind_us": 0.0, "t": {"hbm": 0.0, "dw_alu": 0.0, "pw_tc": 0.0}})
         f["us"] += us
         f["bytes"] += info["dram_bytes"]
         f["n"] += 1
+        t = {"hbm": info["dram_bytes"] / (hbm_peak * 1e3),
+             "dw_alu": info.get("dw_macs", 0) / dw_mac_s * 1e6,
+             "pw_tc": (info.get("pw_macs", 0) + info.get("redundant_macs", 0) + info.get("macs", 0)) / tc_mac_s * 1e6}
+        f["bind_us"] += max(t.values())
+        for kk in t:
+            f["t"][kk] += t[kk]
         rows.append({"op": info["op"], "layers": info["layers"], "tile": info.get("tile"), "us": round(us, 3),
                      "dram_bytes": info["dram_bytes"], "l2_bytes": info["l2_bytes"],
                      "lbl_dram_bytes": info["lbl_dram_bytes"],
@@ -494,6 +506,11 @@ def main():
                          "traffic": traffic_from_profiles(dom, config_tag),
                          "share_of_step": round(d["us"] / sum_us, 3), "launches_per_step": d["n"],
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")},
+            "binding_roof": {"kernel": dom, "t_us": {kk: round(v, 2) for kk, v in d["t"].items()},
+                             "bound": max(d["t"], key=d["t"].get), "measured_us": round(d["us"], 2),
+                             "frac": round(d["bind_us"] / d["us"], 4),
+                             "peaks": {"hbm_gbs": hbm_peak, "dw_fp32_tmac_s": round(dw_mac_s / 1e12, 1),
+                                       "pw_tc_tmac_s": round(tc_mac_s / 1e12, 1)}},
             "stack_hbm": {"achieved_gbs": round(plan["totals"]["dram_bytes"] / (ms_per_step * 1e-3) / 1e9, 1),
                           "frac": round(plan["totals"]["dram_bytes"] / (ms_per_step * 1e-3) / 1e9 / hbm_peak, 4)},
             "e2e": {"value": round(ws * args.batch * e2e_steps / (t_e2e / 1e3), 1), "unit": "images/s",
