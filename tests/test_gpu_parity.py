@@ -212,3 +212,24 @@ def test_pwpw_unsupported_cases_fail_loudly():
         Case("pwpw", "f32", 1, 4, 4, 16, 16, c_mid=16).check()
     with pytest.raises(FcmError, match="UNSUPPORTED"):
         Case("pwpw", "bf16", 1, 4, 4, 16, 16, c_mid=160).check()
+
+
+@pytest.mark.parametrize("act,zp_out,qmin,shift_drop", [(0, 0, -128, 0), (2, 0, 0, 10), (0, 7, -100, 0),
+                                                        (1, 0, 0, 12), (0, -3, -128, 9), (0, 0, -128, 7)])
+@pytest.mark.parametrize("s,tile", [(1, None), (1, {"tile_h": 5, "tile_w": 7}), (2, {"tile_h": 3, "tile_w": 9})])
+def test_dw_int8_pair_core_requant_and_clamp_paths(act, zp_out, qmin, shift_drop, s, tile):
+    """The int8 FFMA2 DW core (dw3_pair_i8): saturating-pack clamps (qmin -128 / 0), the generic
+    clamp (other qmin, nonzero zp_out), the 64-bit requantiser (shifts <= 32, obtained by dropping
+    the shift and the multiplier by the same power of two), and odd tile widths whose last column
+    pair is half dead. Bit-exact against the oracle."""
+    import numpy as np
+    c = Case("dw", "s8", 2, 19, 23, 96, k=3, s=s, tile=tile, act_dw=act)
+    p = c.pd
+    p["zp_out"], p["qmin"] = zp_out, qmin
+    if shift_drop:
+        sh = np.asarray(p["shift_q"], dtype=np.int64)
+        m = np.asarray(p["mult_q"], dtype=np.int64)
+        p["shift_q"] = sh - shift_drop
+        p["mult_q"] = m >> shift_drop
+        assert (p["shift_q"] <= 32).any()
+    c.check()
