@@ -15,6 +15,12 @@ for args, kw in [(("dw", "bf16", 1, 9, 11, 64), {}), (("dw", "s8", 1, 9, 7, 32),
                  # core, PW epilogue groups (96 columns: 2 groups x 2 buffers; 144: 2 groups x 1)
                  (("dwpw", "bf16", 2, 18, 20, 64, 40), {"tile": dict(tile_h=16, tile_w=16)}),
                  (("dwpw", "f16", 1, 15, 13, 24, 16), {"tile": dict(tile_h=14, tile_w=13)}),
-                 (("pw", "bf16", 2, 13, 11, 16, 96), {}), (("pw", "bf16", 2, 13, 11, 24, 144), {})]:
+                 (("pw", "bf16", 2, 13, 11, 16, 96), {}), (("pw", "bf16", 2, 13, 11, 24, 144), {}),
+                 # int8 FFMA2 DW core: narrow pixel (C = 32 staged at 32 B), odd tile width (the
+                 # last column pair reads S words past the tile into the slack), stride 2; PWPW
+                 (("dw", "s8", 1, 9, 11, 32), {"tile": dict(tile_h=5, tile_w=7)}),
+                 (("dw", "s8", 1, 12, 13, 160), {"s": 2, "tile": dict(tile_h=3, tile_w=5)}),
+                 (("pwpw", "bf16", 1, 9, 11, 32, 48), {"c_mid": 64}),
+                 (("pwpw", "s8", 1, 7, 9, 64, 32), {"c_mid": 48})]:
     Case(*args, **kw).check()
     print("ok", args, kw, flush=True)
