@@ -156,6 +156,52 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
       });
     }
     return;
+  } else if constexpr (DT == FCM_S8 && K >= 5) {
+    // int8 5x5 / 7x7: weights stay packed (one word = 4 channels per tap, K^2 registers) and are
+    // widened at use; each output row re-reads its K x K input words from shared memory. Exact
+    // int32 accumulation (register pressure, not speed: these layers are rare)
+    const int cw_valid = min(32, (C - c0) / 4);
+    const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+    const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+    const int cl = c0 + wd * 4;
+    const bool cval = wd < cw_valid;
+    uint32_t Wp[K][K];
+    {
+      const uint32_t* g = reinterpret_cast<const uint32_t*>(wdw);
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < K; ++j) Wp[i][j] = cval ? __ldg(g + (i * K + j) * (C / 4) + cl / 4) : 0u;
+    }
+    EpiC ec[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) ec[v] = load_epi<DT>(ep, cl + v, cval);
+    mbar_wait(&bar, 0);
+    for (int cb = warp * npix; cb < tw; cb += 4 * npix) {
+      const int col = cb + grp;
+      const int x = x0 + col;
+      const bool live = col < tw && x < Wo && cval;
+      const uint32_t src = smem_u32(xs) + (((live ? col : cb) * S) * pwd + wd) * 4;
+      for (int yy = 0; yy < nrows; ++yy) {
+        int32_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const uint32_t rp = src + min(yy * S + i, th_in - 1) * (tw_in * pb);
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const uint32_t xw = lds32(rp + j * pb);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              acc[v] += (static_cast<int32_t>(xw << (24 - 8 * v)) >> 24) *
+                        (static_cast<int32_t>(Wp[i][j] << (24 - 8 * v)) >> 24);
+          }
+        }
+        if (live) {
+          const size_t pix = (static_cast<size_t>(n) * Ho + (y0 + yy)) * Wo + x;
+          yw[(pix * C + cl) / 4] = epi_pack<DT>(acc, ec, ep);
+        }
+      }
+    }
   } else {
     // lane groups as in the pair core: a channel group with fewer valid words than lanes (e.g.
     // int8 C = 32 -> 8 words) packs 2 or 4 output columns into one warp instead of idling lanes
@@ -281,7 +327,9 @@ static int launch_dw_dt(const void* x, const void* wdw, const Epi& ep, void* y, 
   if (g.k == 3 && g.s == 2) return launch_dw_t<DT, 3, 2>(x, wdw, ep, y, g, st);
   if (g.k == 5 && g.s == 1) return launch_dw_t<DT, 5, 1>(x, wdw, ep, y, g, st);
   if (g.k == 5 && g.s == 2) return launch_dw_t<DT, 5, 2>(x, wdw, ep, y, g, st);
-  return set_error(FCM_E_UNSUPPORTED, "dw: only k in {3,5} and stride in {1,2} are built");
+  if (g.k == 7 && g.s == 1) return launch_dw_t<DT, 7, 1>(x, wdw, ep, y, g, st);
+  if (g.k == 7 && g.s == 2) return launch_dw_t<DT, 7, 2>(x, wdw, ep, y, g, st);
+  return set_error(FCM_E_UNSUPPORTED, "dw: only k in {3,5,7} and stride in {1,2} are built");
 }
 
 int launch_dw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {

@@ -319,7 +319,7 @@ static Cost b200_pwdw(const Layer& p, const Layer& d, ll N, int dt, ll b, const 
   } else {
     default_pwdw_tile(g);
     td = 128 / b;
-    if (!pwdw_tile_ok(g, g.nb, g.th, g.tw)) return c;
+    if (!pwdw_tile_ok(g, g.nb, g.th, g.tw) || !pwdw_smem_fits(dt, g)) return c;
   }
   c.ok = true;
   c.nb = g.nb; c.th = g.th; c.tw = g.tw; c.nsplit = cdiv(Cm, td);
@@ -458,6 +458,10 @@ static std::string run(const char* model_json, const char* gpu_json) {
   for (size_t i = 1; i < n; ++i) {
     if (!link[i] || outdeg[i - 1] != 1 || indeg[i] != 1) continue;
     const Layer &a = L[i - 1], &c = L[i];
+    // the fused kernels are built for k in {3, 5} (fcm_dw also has k = 7): no FCM candidate
+    // otherwise in b200 mode (paper mode keeps the paper's decision)
+    const Layer& dwl = a.kind == "dw" ? a : c;
+    if (mode != "paper" && dwl.kind == "dw" && dwl.k != 3 && dwl.k != 5) continue;
     Cost f;
     if (a.kind == "dw" && c.kind == "pw") {
       if (mode == "paper") {

@@ -104,6 +104,22 @@ inline bool pwdw_tile_ok(const Geo& g, int nb, int th, int tw) {
   return nb * th_in * tw_in <= 256 && th_in <= 256 && tw_in <= 256;
 }
 
+// Shared memory of the tensor-core PWDW_R kernel at its minimum configuration (2 X/B stages, 2 T
+// buffers, non-resident B), as its launcher computes it: fixed part = barriers + PW/DW epilogue
+// constants for all C_mid + DW weights of all C_mid slices (grows with C_mid).
+inline bool pwdw_smem_fits(int dt, const Geo& g, int smem_optin = 232448) {
+  const int es = dt == FCM_F32 ? 4 : (dt == FCM_S8 ? 1 : 2);
+  const int td = 128 / es;
+  const int r = g.nb * halo(g.th, g.k, g.s) * halo(g.tw, g.k, g.s);
+  const long mb = (r + 127) / 128, tbytes = ((long)r * 144 + 1023) / 1024 * 1024;
+  const long ncap = (long)(g.Cout + td - 1) / td * td, nslice = ncap / td;
+  const long consts = (dt == FCM_S8 ? 12 : 8) * ncap;
+  const bool pair = (dt == FCM_BF16 || dt == FCM_F16) && g.k == 3;
+  const long wbytes = pair ? 10 * nslice * 32 * 8 : (long)g.k * g.k * nslice * 128;
+  const long fixed = 1024 + 2 * consts + wbytes + 512;
+  return fixed + 2 * tbytes + 2 * (mb * 16384 + td * 128) <= smem_optin;
+}
+
 inline void default_pwdw_tile(Geo& g) {
   long best = -1;
   int bn = 1, bh = 1, bw = 1;

@@ -87,6 +87,28 @@ def cvt13_projections():
     return blocks
 
 
+def proxylessnas_gpu():
+    """the MBConv DW/PW layers of ProxylessNAS-GPU
+    (3x3 / 5x5 / 7x7 DW, expansions 1 / 3 / 6) after the 3x3 s2 stem (112x112x40), + final
+    PW 432->1728. Per-block (expansion, kernel) choices follow the published GPU architecture as
+    recalled without network access (reading R23); SE-free, RELU6."""
+    spec = [(1, 24, 1, 3), (3, 32, 2, 5), (3, 32, 1, 3), (3, 56, 2, 7), (3, 56, 1, 3), (6, 112, 2, 7),
+            (3, 112, 1, 5), (6, 128, 1, 5), (3, 128, 1, 3), (3, 128, 1, 5), (6, 256, 2, 7), (6, 256, 1, 7),
+            (6, 256, 1, 7), (6, 256, 1, 5), (6, 432, 1, 7)]
+    blocks, hw, c = [], 112, 40
+    for t, co, st, k in spec:
+        ho = hw // st
+        b = []
+        if t != 1:
+            b.append(_pw(hw, hw, c, c * t))
+        b.append(_dw(hw, hw, c * t, k, st))
+        b.append(_pw(ho, ho, c * t, co, ACT_NONE))
+        blocks.append(b)
+        hw, c = ho, co
+    blocks.append([_pw(hw, hw, c, 1728)])
+    return blocks
+
+
 def xception():
     """the separable convolutions of Xception at 299x299
     (entry flow after the two stem convs, 8x3 middle flow, exit flow). A separable conv is
@@ -125,6 +147,7 @@ NETWORKS = {
     "efficientnet_b0": efficientnet_b0,
     "cvt13": cvt13_projections,
     "xception": xception,
+    "proxylessnas_gpu": proxylessnas_gpu,
     "ceit_leff": ceit_leff,
     "cmt_irffn": cmt_irffn,
 }

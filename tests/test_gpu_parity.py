@@ -27,7 +27,7 @@ def test_config0_unfused_layers(fmt):
 
 # ---------------------------------------------------------------- DW
 @pytest.mark.parametrize("fmt", ["f32", "bf16", "f16", "s8"])
-@pytest.mark.parametrize("k,s", [(3, 1), (3, 2), (5, 1), (5, 2)])
+@pytest.mark.parametrize("k,s", [(3, 1), (3, 2), (5, 1), (5, 2), (7, 1), (7, 2)])
 def test_dw(fmt, k, s):
     c = 160 if fmt == "s8" else 80
     Case("dw", fmt, 2, 23, 29, c, k=k, s=s).check()

@@ -71,7 +71,8 @@ def test_stride2_hand_table():
 
 
 @pytest.mark.parametrize("k,s,pads", [(3, 1, (1, 1, 1, 1)), (3, 2, (1, 1, 1, 1)), (5, 2, (2, 2, 2, 2)),
-                                      (3, 2, (0, 0, 1, 1)), (5, 1, (1, 2, 3, 0))])
+                                      (3, 2, (0, 0, 1, 1)), (5, 1, (1, 2, 3, 0)), (7, 1, (3, 3, 3, 3)),
+                                      (7, 2, (3, 2, 1, 3))])
 def test_dw_brute_force_int(k, s, pads):
     x = rng.integers(-128, 128, (2, 6, 7, 3))
     w = rng.integers(-127, 128, (k, k, 3))
@@ -91,7 +92,7 @@ def test_pw_brute_force_int():
                           brute_grouped_conv(x.tolist(), wt, 1, 1, (0, 0, 0, 0)))
 
 
-@pytest.mark.parametrize("k,s,p", [(3, 1, 1), (3, 2, 1), (5, 1, 2), (5, 2, 2)])
+@pytest.mark.parametrize("k,s,p", [(3, 1, 1), (3, 2, 1), (5, 1, 2), (5, 2, 2), (7, 1, 3), (7, 2, 3)])
 def test_dw_matches_torch_conv2d_f64(k, s, p):
     x = rng.uniform(-1, 1, (2, 11, 9, 8))
     w = rng.uniform(-1, 1, (k, k, 8))

@@ -14,7 +14,8 @@ CASES = [("single_dwpw", "f32", 1), ("single_dwpw", "s8", 1), ("mobilenet_v1", "
          ("mobilenet_v2", "bf16", 256), ("mobilenet_v2", "bf16", 1), ("efficientnet_b0", "s8", 256),
          ("efficientnet_b0", "s8", 32), ("cvt13", "bf16", 512),
          ("xception", "bf16", 64), ("xception", "s8", 1), ("ceit_leff", "bf16", 256), ("cmt_irffn", "s8", 64),
-         ("cmt_irffn", "bf16", 1)]
+         ("cmt_irffn", "bf16", 1),
+         ("proxylessnas_gpu", "bf16", 64), ("proxylessnas_gpu", "s8", 1)]
 
 
 @pytest.fixture(scope="module")
