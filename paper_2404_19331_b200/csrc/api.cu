@@ -206,8 +206,10 @@ int fcm_dw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const
   Geo g{x->n, x->h, x->w, x->c, Ho, Wo, x->c, geom->k, geom->stride, geom->pad_t, geom->pad_l, 1, 0, 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (x->layout == FCM_NCHW) return launch_dw_nchw(x->dtype, x->data, w_dw, to_epi(ep), y->data, g, st);
-  // channel pitch not a multiple of 16 B: TMA cannot address it -> CUDA-core kernel
-  if (!pitch_ok(x)) return launch_dw_simt(x->dtype, x->data, w_dw, to_epi(ep), y->data, g, st);
+  // channel pitch not a multiple of 4 B: the word-per-lane kernels cannot address it -> CUDA-core
+  // kernel (multiples of 4 but not 16: the tiled kernel stages with cp.async instead of TMA)
+  if (((size_t)x->c * elem_size(x->dtype)) % 4)
+    return launch_dw_simt(x->dtype, x->data, w_dw, to_epi(ep), y->data, g, st);
   default_dw_tile(g, elem_size(x->dtype));
   if (tile) {
     if (tile->tile_h > 0) g.th = tile->tile_h;

@@ -10,13 +10,19 @@
 #include "common.cuh"
 #include "host.h"
 
+#include <cstring>
+
 namespace fcm {
 
-template <int DT, int K, int S>
+// TMA = false: the pixel pitch C * b is not a multiple of 16 bytes (e.g. int8 C = 728), which TMA
+// cannot address; all threads stage the same halo tile with 8- or 4-byte cp.async (zero-filled
+// outside the image and past C) and the compute below is unchanged.
+template <int DT, int K, int S, bool TMA>
 __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CUtensorMap tmx,
                                                       const typename Tr<DT>::T* __restrict__ wdw, Epi ep,
                                                       typename Tr<DT>::T* __restrict__ y, int C, int Ho, int Wo,
-                                                      int pt, int pl, int th, int tw, int tiles_x, int tiles_y, int pb) {
+                                                      int pt, int pl, int th, int tw, int tiles_x, int tiles_y, int pb,
+                                                      const uint8_t* __restrict__ xr, int H, int W, int chunk) {
   pdl_launch();
   pdl_wait();
   constexpr int V = Tr<DT>::VEC;
@@ -32,16 +38,39 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
   const int c0 = blockIdx.y * KC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pwd = pb >> 2;  // staged 32-bit words per pixel (128 B, or C * ES when C is narrower)
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmx);
-    mbar_init(&bar, 1);
-    fence_barrier_init();
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      tma_prefetch_desc(&tmx);
+      mbar_init(&bar, 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&bar, th_in * tw_in * pb);
+      tma_load_4d(xs, &tmx, &bar, c0, tx * tw * S - pl, ty * th * S - pt, n);
+    }
+  } else {
+    constexpr int ES = Tr<DT>::ES;
+    const int cpp = pb / chunk, cbytes = C * ES, gy0 = ty * th * S - pt, gx0 = tx * tw * S - pl;
+    const uint32_t base = smem_u32(xs);
+    for (int i = threadIdx.x; i < th_in * tw_in * cpp; i += blockDim.x) {
+      const int p = i / cpp, q = i - p * cpp;
+      const int iy = p / tw_in, ix = p - iy * tw_in;
+      const int gy = gy0 + iy, gx = gx0 + ix, boff = c0 * ES + q * chunk;
+      const bool v = gy >= 0 && gy < H && gx >= 0 && gx < W && boff < cbytes;
+      const uint8_t* src = v ? xr + ((static_cast<size_t>(n) * H + gy) * W + gx) * cbytes + boff : xr;
+      if (chunk == 8) cp_async_ca<8>(base + p * pb + q * 8, src, v ? 8 : 0);
+      else cp_async_ca<4>(base + p * pb + q * 4, src, v ? 4 : 0);
+    }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar, th_in * tw_in * pb);
-    tma_load_4d(xs, &tmx, &bar, c0, tx * tw * S - pl, ty * th * S - pt, n);
-  }
+  auto wait_x = [&]() {
+    if constexpr (TMA) {
+      mbar_wait(&bar, 0);
+    } else {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+  };
   const int y0 = ty * th, x0 = tx * tw;
   const int nrows = min(th, Ho - y0);
   uint32_t* yw = reinterpret_cast<uint32_t*>(y);
@@ -60,7 +89,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     const uint64_t sc2 = f2_pack(cval ? (ep.scale ? ep.scale[cl] : 1.f) : 0.f, cval ? (ep.scale ? ep.scale[cl + 1] : 1.f) : 0.f);
     const uint64_t bi2 = f2_pack(cval && ep.bias ? ep.bias[cl] : 0.f, cval && ep.bias ? ep.bias[cl + 1] : 0.f);
     const uint32_t lo_c = bound2<DT>(act_lo(ep.act)), hi_c = bound2<DT>(act_hi(ep.act));
-    mbar_wait(&bar, 0);
+    wait_x();
     const int nseg = (nrows + kSeg - 1) / kSeg;
     const int ncolg = (tw + npix - 1) / npix;
     for (int item = warp; item < ncolg * nseg; item += 4) {
@@ -113,7 +142,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
       bias[1] = f2_pack(b[2], b[3]);
     }
     const int zp = ep.zp_out, qmin = ep.qmin, qmax = ep.qmax;
-    mbar_wait(&bar, 0);
+    wait_x();
     const int nseg = (nrows + kSeg - 1) / kSeg;
     const int ncolp = (tw + 1) / 2;
     const int ncolg = (ncolp + npix - 1) / npix;
@@ -176,7 +205,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     EpiC ec[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) ec[v] = load_epi<DT>(ep, cl + v, cval);
-    mbar_wait(&bar, 0);
+    wait_x();
     for (int cb = warp * npix; cb < tw; cb += 4 * npix) {
       const int col = cb + grp;
       const int x = x0 + col;
@@ -214,7 +243,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     EpiC ec[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) ec[v] = load_epi<DT>(ep, cl + v, cl + v < C);
-    mbar_wait(&bar, 0);
+    wait_x();
     for (int cb = warp * npix; cb < tw; cb += 4 * npix) {
       const int col = cb + grp;
       const int x = x0 + col;
@@ -297,27 +326,34 @@ static int launch_dw_t(const void* x, const void* wdw, const Epi& ep, void* y, c
   constexpr int KC = 128 / ES;
   const int th = g.th, tw = g.tw;
   const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
-  if (th_in > 256 || tw_in > 256) return set_error(FCM_E_INFEASIBLE, "dw tile halo exceeds the TMA box limit (256)");
+  const int cbytes = g.C * ES;
+  const bool tma = cbytes % 16 == 0;
+  if (tma && (th_in > 256 || tw_in > 256)) return set_error(FCM_E_INFEASIBLE, "dw tile halo exceeds the TMA box limit (256)");
   CUtensorMap tm;
-  const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
-  const uint64_t strides[3] = {(uint64_t)g.C * ES, (uint64_t)g.W * g.C * ES, (uint64_t)g.H * g.W * g.C * ES};
-  // channel box: one 128-byte group, or the whole (16-byte multiple) pixel when C is narrower --
-  // no out-of-bounds fill traffic and 4x less shared memory for e.g. int8 C = 32
-  const int pb = (g.C * ES < 128) ? g.C * ES : 128;
-  const uint32_t box[4] = {(uint32_t)(pb / ES), (uint32_t)tw_in, (uint32_t)th_in, 1};
-  if (!encode_tmap(&tm, tmap_dtype(DT), 4, x, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
-    return set_error(FCM_E_CUDA, "cuTensorMapEncodeTiled failed for the DW input");
+  // channel box: one 128-byte group, or the whole pixel when C is narrower -- no out-of-bounds
+  // fill traffic and 4x less shared memory for e.g. int8 C = 32. Without TMA (pitch not a
+  // multiple of 16 B) the narrow pixel is staged at its 16-byte-rounded width.
+  const int pb = cbytes < 128 ? (cbytes + 15) / 16 * 16 : 128;
+  if (tma) {
+    const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
+    const uint64_t strides[3] = {(uint64_t)g.C * ES, (uint64_t)g.W * g.C * ES, (uint64_t)g.H * g.W * g.C * ES};
+    const uint32_t box[4] = {(uint32_t)(pb / ES), (uint32_t)tw_in, (uint32_t)th_in, 1};
+    if (!encode_tmap(&tm, tmap_dtype(DT), 4, x, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return set_error(FCM_E_CUDA, "cuTensorMapEncodeTiled failed for the DW input");
+  } else {
+    memset(&tm, 0, sizeof(tm));
+  }
   const int tiles_x = (g.Wo + tw - 1) / tw, tiles_y = (g.Ho + th - 1) / th;
   // + 2 columns of slack: the int8 column-pair core reads S extra input words past the last
   // column of an odd-width tile (its second output column is dead, never stored)
   const size_t smem = (size_t)th_in * tw_in * pb + 256;
   if (smem > (size_t)device_props().smem_optin) return set_error(FCM_E_INFEASIBLE, "dw tile exceeds shared memory");
-  auto kern = dw_nhwc_kernel<DT, K, S>;
+  auto kern = tma ? dw_nhwc_kernel<DT, K, S, true> : dw_nhwc_kernel<DT, K, S, false>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(tiles_x * tiles_y * g.N, (g.C + KC - 1) / KC);
   using TT = typename Tr<DT>::T;
   launch_k(kern, dim3(grid), dim3(128), smem, st, tm, static_cast<const TT*>(wdw), ep, static_cast<TT*>(y), g.C, g.Ho, g.Wo, g.pt, g.pl,
-                                th, tw, tiles_x, tiles_y, pb);
+           th, tw, tiles_x, tiles_y, pb, static_cast<const uint8_t*>(x), g.H, g.W, cbytes % 8 == 0 ? 8 : 4);
   return check_launch("dw_nhwc_kernel");
 }
 

@@ -250,7 +250,7 @@ static Cost b200_dw(const Layer& d, ll N, int dt, ll b, const Gpu& gp) {
   c.op = "dw";
   Geo g = geo_of(d, N, d.C);
   default_dw_tile(g, (int)b);
-  if (!aligned16(d.C, b)) { g.th = 1; g.tw = 1; }  // element-wise SIMT kernel: unit = one pixel
+  if ((d.C * b) % 4) { g.th = 1; g.tw = 1; }  // element-wise SIMT kernel: unit = one pixel
   c.th = g.th; c.tw = g.tw;
   const Units u = units("dw", N, d, d.C, d.C, 1, g.th, g.tw, aligned16(d.C, b) ? 128 / b : d.C);
   c.l2 = u.total() * b;

@@ -233,3 +233,14 @@ def test_dw_int8_pair_core_requant_and_clamp_paths(act, zp_out, qmin, shift_drop
         p["mult_q"] = m >> shift_drop
         assert (p["shift_q"] <= 32).any()
     c.check()
+
+
+@pytest.mark.parametrize("fmt,c", [("s8", 728), ("s8", 40), ("s8", 12), ("bf16", 36), ("bf16", 6), ("f32", 5),
+                                   ("f16", 30)])
+@pytest.mark.parametrize("k,s", [(3, 1), (3, 2), (5, 1), (7, 2)])
+def test_dw_cp_async_staging_unaligned_pitch(fmt, c, k, s):
+    """Pixel pitches that are multiples of 4 (8) bytes but not 16 (Xception int8 C = 728): the
+    tiled DW kernel stages the halo with cp.async instead of TMA, zero-filling outside the image
+    and past C; the cores are unchanged (int8 bit-exact, floats within tolerance)."""
+    Case("dw", fmt, 2, 11, 13, c, k=k, s=s).check()
+    Case("dw", fmt, 1, 9, 10, c, k=k, s=s, tile={"tile_h": 3, "tile_w": 5}).check()
