@@ -607,6 +607,74 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           else if (seg_sel == 7) run_act(std::integral_constant<int, 7>(), dv.n7);
           else run_act(std::integral_constant<int, 4>(), dv.n4);
         } else {
+         bool done = false;
+         if constexpr (DT == FCM_S8 && K == 3) {
+          // int8: the exact column-pair FFMA2 core of the LBL DW (dw3_pair_i8), same lane groups;
+          // a lane owns one word (4 channels) of two adjacent columns, rows stored to the SW128 A
+          // tile. Chunks with <= 8 valid words (C_in = 32) stay on the per-column core (faster there).
+          const int cw_valid = min(32, (Cin - kc * KC + 3) / 4);
+          if (cw_valid > 8) {
+          done = true;
+          const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+          const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+          const int cl = kc * KC + wd * 4;
+          uint64_t Wf[9][2], bias[2];
+          RqI8 rq[4];
+          {
+            const uint32_t wa = smem_u32(wsm) + 4 * (kc * 32 + wd);
+#pragma unroll
+            for (int t9 = 0; t9 < 9; ++t9) {
+              const uint32_t w = lds32(wa + 4 * t9 * nk * 32);
+              float f[4];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) f[v] = static_cast<float>(static_cast<int32_t>(w << (24 - 8 * v)) >> 24);
+              Wf[t9][0] = f2_pack(f[0], f[1]);
+              Wf[t9][1] = f2_pack(f[2], f[3]);
+            }
+            float bf[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const EpiC e = epic<DT>(dcs, cl + v);
+              bf[v] = static_cast<float>(e.bq);
+              rq[v] = make_rq(e.m, e.sh < 1 ? 40 : e.sh);
+            }
+            bias[0] = f2_pack(bf[0], bf[1]);
+            bias[1] = f2_pack(bf[2], bf[3]);
+          }
+          const int zp = ed.zp_out, qmin = ed.qmin, qmax = ed.qmax;
+          named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
+          const int ncolp = (tw + 1) >> 1;
+          const int ncg = (nb * ncolp + npix - 1) / npix;
+          for (int item = dw; item < ncg * nseg; item += kDwpwNDW) {
+            const int cg = item / nseg, seg = item - cg * nseg;
+            const int cpr = cg * npix + grp;
+            const bool live = cpr < nb * ncolp;
+            const int cpi = live ? cpr : cg * npix;
+            const int b = cpi / ncolp, x0 = 2 * (cpi - b * ncolp);
+            const int y0 = seg * kSeg;
+            const int nvalid = live ? th - y0 : 0;
+            const bool c1 = x0 + 1 < tw;
+            const uint32_t src = st + (((b * th_in) * tw_in + x0 * S) * 32 + wd) * 4;
+            dw3_pair_i8<S, kSeg>(src, 128, tw_in * 128, y0, th_in - 1, Wf, bias, [&](int r, const uint64_t (&acc)[2][2]) {
+              if (r < nvalid) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                  int32_t v[4];
+                  f2_to_i2(acc[c][0], v[0], v[1]);
+                  f2_to_i2(acc[c][1], v[2], v[3]);
+                  uint32_t word = 0;
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+                    word |= (static_cast<uint32_t>(min(max(rq_apply(v[q], rq[q]) + zp, qmin), qmax)) & 0xFFu) << (8 * q);
+                  const int m = (b * th + y0 + r) * tw + x0 + c;
+                  if (c == 0 || c1) sts32(abase + sw128_off(m, wd), cl < Cin ? word : 0u);
+                }
+              }
+            });
+          }
+          }
+         }
+         if (!done) {
           DwW<DT, K> W;
           // lane groups (as in the pair core): a partly filled channel chunk packs 2 or 4 output
           // columns into one warp; lanes past the valid words compute with zero weights and their
@@ -636,6 +704,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
                                    if (live) sts32(abase + sw128_off(m, wd), word);
                                  });
           }
+         }
         }
         if (!(dbg & 64)) fence_proxy_async_smem();
         __syncwarp();
