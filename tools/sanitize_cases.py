@@ -21,6 +21,11 @@ for args, kw in [(("dw", "bf16", 1, 9, 11, 64), {}), (("dw", "s8", 1, 9, 7, 32),
                  (("dw", "s8", 1, 9, 11, 32), {"tile": dict(tile_h=5, tile_w=7)}),
                  (("dw", "s8", 1, 12, 13, 160), {"s": 2, "tile": dict(tile_h=3, tile_w=5)}),
                  (("pwpw", "bf16", 1, 9, 11, 32, 48), {"c_mid": 64}),
-                 (("pwpw", "s8", 1, 7, 9, 64, 32), {"c_mid": 48})]:
+                 (("pwpw", "s8", 1, 7, 9, 64, 32), {"c_mid": 48}),
+                 # int8 FFMA2 core inside DWPW (full and partial chunks); cp.async-staged DW
+                 # (pixel pitch not a multiple of 16 B) incl. k = 7
+                 (("dwpw", "s8", 1, 9, 11, 160, 64), {}), (("dwpw", "s8", 1, 12, 13, 128, 32), {"s": 2}),
+                 (("dw", "s8", 1, 7, 9, 728), {}), (("dw", "bf16", 1, 9, 8, 36), {"k": 7, "s": 2}),
+                 (("dw", "s8", 1, 9, 9, 40), {"k": 7})]:
     Case(*args, **kw).check()
     print("ok", args, kw, flush=True)
