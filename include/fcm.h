@@ -123,7 +123,11 @@ typedef struct {
   int32_t tile_h, tile_w, tile_n, c_chunk, n_split;
 } fcm_tile;
 
-/* Layer-by-layer depthwise conv. x [N,H,W,C], w_dw [k][k][C], y [N,Ho,Wo,C]. */
+/* Layer-by-layer depthwise conv. x [N,H,W,C], w_dw [k][k][C], y [N,Ho,Wo,C].
+ * k in {3, 5, 7}, stride in {1, 2} (else FCM_E_UNSUPPORTED). NHWC pixel pitch C * elem:
+ * a multiple of 16 B -> TMA-staged tiles; a multiple of 4 B -> the same tiles staged with
+ * cp.async; otherwise an element-wise CUDA-core kernel. The fused calls (fcm_dwpw,
+ * fcm_pwdw_r) are built for k in {3, 5}. */
 int fcm_dw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const fcm_epilogue* ep,
            fcm_tensor* y, const fcm_tile* tile, void* stream);
 
