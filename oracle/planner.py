@@ -176,13 +176,14 @@ def pw_units(M, ci, co, bm, bn):
 
 
 DEFAULT_GPU = dict(num_sms=148, smem_bytes=232448, hbm_gbs=6534.5, l2_gbs=20000.0, tc_tmacs=832.0,
-                   ffma_tmacs=37.2, dw_eff=0.5, launch_us=2.0)
+                   ffma_tmacs=37.2, dw_eff=0.5, launch_us=2.0, dw_eff_i8=0.17, dw_eff_i8_fused=0.085)
 
 
 def pred_us(c, dtype, g):
     hbm = c["dram_bytes"] / (g["hbm_gbs"] * 1e3)
     l2 = c["l2_bytes"] / (g["l2_gbs"] * 1e3)
-    dw = c["dw_macs"] / (g["ffma_tmacs"] * 1e6 * g["dw_eff"])
+    eff = (g["dw_eff_i8"] if c["op"] == "dw" else g["dw_eff_i8_fused"]) if dtype == "s8" else g["dw_eff"]
+    dw = c["dw_macs"] / (g["ffma_tmacs"] * 1e6 * eff)
     tcr = g["ffma_tmacs"] if dtype == "f32" else (2.0 if dtype == "s8" else 1.0) * g["tc_tmacs"]
     pw = c["pw_macs"] / (tcr * 1e6)
     return max(max(hbm, l2), max(dw, pw)) + g["launch_us"]

@@ -40,6 +40,9 @@ struct Layer {
 struct Gpu {
   ll sms = 148, smem = 232448, l2 = 126LL << 20;
   double hbm_gbs = 6534.5, l2_gbs = 20000, tc_tmacs = 832, ffma_tmacs = 37.2, dw_eff = 0.5, launch_us = 2.0;
+  // int8 DW efficiency (of the FFMA peak), measured on B200: LBL FFMA2 core ~0.17, inside the fused
+  // kernels ~0.085 (profiles/r01_ncu_summary.md)
+  double dw_eff_i8 = 0.17, dw_eff_i8_fused = 0.085;
 };
 
 // ---------------------------------------------------------------------------- Eq. 1-4 (verbatim)
@@ -227,7 +230,8 @@ struct Cost {
 static double t_us(const Cost& c, int dt, const Gpu& g) {
   const double hbm = c.dram / (g.hbm_gbs * 1e3);
   const double l2 = c.l2 / (g.l2_gbs * 1e3);
-  const double dw = c.dw_macs / (g.ffma_tmacs * 1e6 * g.dw_eff);
+  const double eff = dt == FCM_S8 ? (c.op == "dw" ? g.dw_eff_i8 : g.dw_eff_i8_fused) : g.dw_eff;
+  const double dw = c.dw_macs / (g.ffma_tmacs * 1e6 * eff);
   const double tcr = (dt == FCM_F32) ? g.ffma_tmacs : (dt == FCM_S8 ? 2.0 : 1.0) * g.tc_tmacs;
   const double pw = c.pw_macs / (tcr * 1e6);
   return std::max(std::max(hbm, l2), std::max(dw, pw)) + g.launch_us;
@@ -404,6 +408,8 @@ static std::string run(const char* model_json, const char* gpu_json) {
     gp.tc_tmacs = g.num("tc_tmacs", gp.tc_tmacs);
     gp.ffma_tmacs = g.num("ffma_tmacs", gp.ffma_tmacs);
     gp.dw_eff = g.num("dw_eff", gp.dw_eff);
+    gp.dw_eff_i8 = g.num("dw_eff_i8", gp.dw_eff_i8);
+    gp.dw_eff_i8_fused = g.num("dw_eff_i8_fused", gp.dw_eff_i8_fused);
     gp.launch_us = g.num("launch_us", gp.launch_us);
   }
   const Value* lv = m.get("layers");
