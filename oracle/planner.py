@@ -5,9 +5,15 @@ paper mode: the paper's procedure written out plainly: for every lay
   >= #SMs -- waived when unsatisfiable, reading R17); for every adjacent single-consumer pair,
   minimise the FCM equation (Eq. 4 for PW->DW, the constructed DWPW equation for DW->PW); keep a
   pair iff FCM < LBL sum; choose non-overlapping pairs by a chain DP.
-b200 mode: re-derive every candidate the library reports -- compulsory HBM bytes, exact unit
-  counts at the reported tile (counting.*_units), MACs and the predicted time -- and re-run the
-  decision + DP from those numbers.
+  Every GMA value comes from the pinned equation functions of oracle/counting.py (Eq. 1
+  overlap, Eq. 2 pw_gma, Eq. 3 dw_gma, Eq. 4 pwdw_gma, the constructed dwpw_gma); only the grid
+  and the two constraints are written here. A layer whose grid is empty (no tile fits on chip)
+  is left untiled: one tile, GMA = IFM + W + OFM (the single-tile closed form).
+b200 mode: re-derive, from the candidate's reported tile (images x rows x cols per tile, number
+  of channel splits), its compulsory HBM bytes (counting.compulsory), its exact L2->SM element
+  counts (exact unit enumeration) and its MACs; re-run the decision rule and the chain
+  DP on the library's reported times. The time model itself is not mirrored here: it
+  is checked against measured kernel times (tests/test_planner_time_model.py).
 Grid (reading R18): spatial {1,2,4,8,16,32,64, n, divisors of n <= 64} within [1, n]; depth
   {multiples of 32 <= D} U {D}; enumeration order (td, th, tw), first minimum wins; for PW->DW a
   full-map tile (PWDW, no redundancy) wins ties against PWDW_R.
@@ -16,7 +22,7 @@ from __future__ import annotations
 
 from math import ceil
 
-from oracle.counting import overlap, tiles_1d, touched
+from oracle.counting import compulsory, dw_gma, dwpw_gma, overlap, pw_gma, pwdw_gma, tiles_1d, touched
 
 ESZ = {"f32": 4, "bf16": 2, "f16": 2, "s8": 1}
 
@@ -38,6 +44,7 @@ def out_hw(l):
 
 
 def _search(fn, sms):
+    """#OFM tiles >= #SMs, waived when unsatisfiable (reading R17)."""
     best = fn(sms)
     return best if best is not None else fn(1)
 
@@ -58,12 +65,12 @@ def paper_dw(l, N, b, sms, smem):
                     thi, twi = min((th - 1) * s + k, H), min((tw - 1) * s + k, W)
                     if (thi * twi * td + th * tw * td + k * k * td) * b > smem:
                         continue
-                    ov = overlap(H, W, th * s, tw * s, k, k, s)          # Eq. 1
-                    gma = 2 * C * N * ov + N * H * W * C + N * Ho * Wo * C + ceil(N * Ho * Wo / (th * tw)) * k * k * C
-                    if best is None or gma < best[0]:                    # Eq. 3
+                    ov = N * overlap(H, W, th * s, tw * s, k, k, s)      # Eq. 1, every image
+                    gma = dw_gma(C, ov, N * H * W * C, N * Ho * Wo * C, N * Ho * Wo, th * tw, k * k * C)  # Eq. 3
+                    if best is None or gma < best[0]:
                         best = (gma, th, tw, td, "dw")
         return best
-    return _search(run, sms)
+    return _search(run, sms) or (N * H * W * C + k * k * C + N * Ho * Wo * C, Ho, Wo, C, "dw")
 
 
 def paper_pw(l, N, b, sms, smem):
@@ -80,12 +87,11 @@ def paper_pw(l, N, b, sms, smem):
                         continue
                     if (th * tw * Ci + th * tw * td + td * Ci) * b > smem:
                         continue
-                    gma = ceil(Ci * Co / (td * Ci)) * N * H * W * Ci + N * H * W * Co + \
-                        ceil(N * H * W * Co / (th * tw * td)) * Ci * Co    # Eq. 2
+                    gma = pw_gma(N * H * W * Ci, N * H * W * Co, Ci * Co, td * Ci, th * tw * td)  # Eq. 2
                     if best is None or gma < best[0]:
                         best = (gma, th, tw, td, "pw")
         return best
-    return _search(run, sms)
+    return _search(run, sms) or (N * H * W * Ci + Ci * Co + N * H * W * Co, H, W, Co, "pw")
 
 
 def paper_pwdw(p, d, N, b, sms, smem):
@@ -105,10 +111,9 @@ def paper_pwdw(p, d, N, b, sms, smem):
                     thi, twi = min((th - 1) * s + k, H), min((tw - 1) * s + k, W)
                     if (thi * twi * Ci + th * tw * td + td * Ci + k * k * td + thi * twi * td) * b > smem:
                         continue
-                    ov = overlap(H, W, th * s, tw * s, k, k, s)
-                    rep = max(ceil(Ci * Cm / (td * Ci)), ceil(k * k * Cm / (k * k * td)))
-                    gma = (2 * Ci * N * ov + N * H * W * Ci) * rep + ceil(N * Ho * Wo * Cm / (th * tw * td)) * Ci * Cm + \
-                        ceil(N * Ho * Wo / (th * tw)) * k * k * Cm + N * Ho * Wo * Cm   # Eq. 4 + store
+                    ov = N * overlap(H, W, th * s, tw * s, k, k, s)
+                    gma = pwdw_gma(Ci, ov, N * H * W * Ci, Ci * Cm, td * Ci, k * k * Cm, k * k * td,
+                                   N * Ho * Wo * Cm, th * tw * td, N * Ho * Wo, th * tw)   # Eq. 4 + DwOFM (R15)
                     kind = "pwdw" if (th == Ho and tw == Wo) else "pwdw_r"
                     if best is None or gma < best[0] or (gma == best[0] and kind == "pwdw" and best[4] == "pwdw_r"):
                         best = (gma, th, tw, td, kind)
@@ -133,112 +138,84 @@ def paper_dwpw(d, p, N, b, sms, smem):
                     thi, twi = min((th - 1) * s + k, H), min((tw - 1) * s + k, W)
                     if (thi * twi * Ci + th * tw * td + k * k * Ci + Ci * td + th * tw * Ci) * b > smem:
                         continue
-                    ov = overlap(H, W, th * s, tw * s, k, k, s)
-                    nw = ceil(Ci * Co / (Ci * td))
-                    gma = (2 * Ci * N * ov + N * H * W * Ci) * nw + ceil(N * Ho * Wo / (th * tw)) * nw * k * k * Ci + \
-                        ceil(N * Ho * Wo * Co / (th * tw * td)) * Ci * Co + N * Ho * Wo * Co
+                    ov = N * overlap(H, W, th * s, tw * s, k, k, s)
+                    gma = dwpw_gma(Ci, ov, N * H * W * Ci, k * k * Ci, Ci * Co, Ci * td, N * Ho * Wo * Co,
+                                   th * tw * td, N * Ho * Wo, th * tw)   # constructed (R13)
                     if best is None or gma < best[0]:
                         best = (gma, th, tw, td, "dwpw")
         return best
     return _search(run, sms)
 
 
-# ------------------------------------------------------------------ B200 byte / MAC model
-def units(kind, N, d, c_in, c_x, nb, th, tw, sl):
-    """Exact unit enumeration: unit = nb images x th x tw output tile x channel slice `sl`."""
+# ------------------------------------------------------------------ B200 byte / MAC accounting
+def units(kind, N, d, c_in, c_x, nb, th, tw, ns):
+    """Exact unit enumeration of a B200 kernel launch (reading R21): a unit = nb images x th x tw
+    output tile x one of `ns` channel splits (of C_out for dwpw, of C_mid for pwdw; dw units
+    cover every channel). Every unit loads its clipped input halo (padding is never fetched) --
+    over ALL C_in channels for the fused kinds -- its weights, and stores its outputs once.
+    Counts are in elements; the split widths sum to the channel count, so only `ns` matters."""
     Ho, Wo = out_hw(d)
     pt, pl = d.get("pads", [d["k"] // 2] * 4)[:2]
-    cs = c_in if kind == "dw" else c_x
+    k = d["k"]
     ifm = w = halo = 0
     for n0 in range(0, N, nb):
         nbe = min(nb, N - n0)
         for (y0, y1) in tiles_1d(Ho, th):
-            ny = touched(y0, y1, d["k"], d["stride"], pt, d["h"])
+            ny = touched(y0, y1, k, d["stride"], pt, d["h"])
             for (x0, x1) in tiles_1d(Wo, tw):
-                nx = touched(x0, x1, d["k"], d["stride"], pl, d["w"])
-                for (c0, c1) in tiles_1d(cs, sl):
-                    ce, px = c1 - c0, nbe * ny * nx
-                    if kind == "dw":
-                        ifm += px * ce
-                        w += d["k"] ** 2 * ce
-                    elif kind == "dwpw":
-                        ifm += px * c_in
-                        w += d["k"] ** 2 * c_in + c_in * ce
-                    else:
-                        ifm += px * c_in
-                        w += c_in * ce + d["k"] ** 2 * ce
-                        halo += px * ce
-    return {"ifm": ifm, "w": w, "ofm": N * Ho * Wo * cs, "halo": halo}
+                px = nbe * ny * touched(x0, x1, k, d["stride"], pl, d["w"])
+                if kind == "dw":
+                    ifm += px * c_in
+                    w += k * k * c_in
+                elif kind == "dwpw":
+                    ifm += ns * px * c_in
+                    w += ns * k * k * c_in + c_in * c_x
+                else:
+                    ifm += ns * px * c_in
+                    w += c_in * c_x + k * k * c_x
+                    halo += px * c_x
+    return {"ifm": ifm, "w": w, "ofm": N * Ho * Wo * (c_in if kind == "dw" else c_x), "halo": halo}
 
 
-def pw_units(M, ci, co, bm, bn):
-    return {"ifm": ceil(co / bn) * M * ci, "w": ceil(M / bm) * co * ci, "ofm": M * co}
-
-
-DEFAULT_GPU = dict(num_sms=148, smem_bytes=232448, hbm_gbs=6534.5, l2_gbs=20000.0, tc_tmacs=832.0,
-                   ffma_tmacs=37.2, dw_eff=0.5, launch_us=2.0, dw_eff_i8=0.17, dw_eff_i8_fused=0.085)
-
-
-def pred_us(c, dtype, g):
-    hbm = c["dram_bytes"] / (g["hbm_gbs"] * 1e3)
-    l2 = c["l2_bytes"] / (g["l2_gbs"] * 1e3)
-    eff = (g["dw_eff_i8"] if c["op"] == "dw" else g["dw_eff_i8_fused"]) if dtype == "s8" else g["dw_eff"]
-    dw = c["dw_macs"] / (g["ffma_tmacs"] * 1e6 * eff)
-    tcr = g["ffma_tmacs"] if dtype == "f32" else (2.0 if dtype == "s8" else 1.0) * g["tc_tmacs"]
-    pw = c["pw_macs"] / (tcr * 1e6)
-    return max(max(hbm, l2), max(dw, pw)) + g["launch_us"]
-
-
-def _bn(co, ns, b):
-    """PW column block of the tensor-core kernels: one block padded to 16 when ns == 1, else a
-    multiple of the 128-byte store chunk (128/b columns), at most 256."""
-    if ns == 1:
-        return (co + 15) // 16 * 16
-    cpc = 128 // b
-    return min((ceil(co / ns) + cpc - 1) // cpc * cpc, 256)
-
-
-def _simt(dtype, b, *chans):
-    """fp32 and any NHWC pitch that is not a multiple of 16 bytes run on the CUDA-core kernels."""
-    return dtype == "f32" or any((c * b) % 16 for c in chans)
+def pw_units(M, ci, co, bm, ns):
+    """PW launch: row blocks of bm pixels x ns column splits; each block reads its A rows once
+    per split and the weights once per row block."""
+    return {"ifm": ns * M * ci, "w": ceil(M / bm) * co * ci, "ofm": M * co}
 
 
 def b200_numbers(op, layers, N, dtype, tile):
-    """Compulsory HBM bytes, exact L2->SM bytes and MACs of one candidate at its reported tile."""
+    """Compulsory HBM bytes, exact L2->SM bytes and MACs of one candidate at the
+    tile it reports (tile_n, tile_h, tile_w, n_split)."""
     b = ESZ[dtype]
     nb, th, tw, ns = tile["tile_n"], tile["tile_h"], tile["tile_w"], tile["n_split"]
     if op == "dw":
         d = layers[0]
         Ho, Wo = out_hw(d)
-        u = units("dw", N, d, d["c"], d["c"], 1, th, tw, d["c"] if (d["c"] * b) % 16 else 128 // b)
-        dram = (N * (d["h"] * d["w"] * d["c"] + Ho * Wo * d["c"]) + d["k"] ** 2 * d["c"]) * b
-        return dict(dram_bytes=dram, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
+        u = units("dw", N, d, d["c"], d["c"], 1, th, tw, 1)
+        return dict(dram_bytes=compulsory("dw", N, d["h"], d["w"], d["c"], d["c"], d["k"], d["stride"]) * b,
+                    l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
                     dw_macs=N * Ho * Wo * d["c"] * d["k"] ** 2, pw_macs=0, redundant_macs=0)
     if op == "pw":
         p = layers[0]
         M = N * p["h"] * p["w"]
         ci, co = p["c_in"], p["c_out"]
-        bm = th
-        bn = 64 if _simt(dtype, b, ci, co) else _bn(co, ns, b)
-        u = pw_units(M, ci, co, bm, bn)
-        return dict(dram_bytes=(M * (ci + co) + ci * co) * b, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
-                    dw_macs=0, pw_macs=M * ci * co, redundant_macs=0)
+        u = pw_units(M, ci, co, th, ns)
+        return dict(dram_bytes=compulsory("pw", N, p["h"], p["w"], ci, co) * b,
+                    l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b, dw_macs=0, pw_macs=M * ci * co, redundant_macs=0)
     if op == "dwpw":
         d, p = layers
         Ho, Wo = out_hw(d)
         ci, co = d["c"], p["c_out"]
-        bn = 64 if _simt(dtype, b, ci, co) else _bn(co, ns, b)
-        u = units("dwpw", N, d, ci, co, nb, th, tw, bn)
-        dram = (N * (d["h"] * d["w"] * ci + Ho * Wo * co) + d["k"] ** 2 * ci + ci * co) * b
-        return dict(dram_bytes=dram, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
+        u = units("dwpw", N, d, ci, co, nb, th, tw, ns)
+        return dict(dram_bytes=compulsory("dwpw", N, d["h"], d["w"], ci, co, d["k"], d["stride"]) * b,
+                    l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b,
                     dw_macs=N * Ho * Wo * ci * d["k"] ** 2 * ns, pw_macs=N * Ho * Wo * ci * co, redundant_macs=0)
     p, d = layers
     Ho, Wo = out_hw(d)
     ci, cm = p["c_in"], p["c_out"]
-    td = 32 if _simt(dtype, b, ci, cm) else 128 // b
-    u = units("pwdw", N, d, ci, cm, nb, th, tw, td)
-    dram = (N * (d["h"] * d["w"] * ci + Ho * Wo * cm) + ci * cm + d["k"] ** 2 * cm) * b
-    return dict(dram_bytes=dram, l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b, dw_macs=N * Ho * Wo * cm * d["k"] ** 2,
+    u = units("pwdw", N, d, ci, cm, nb, th, tw, ns)
+    return dict(dram_bytes=compulsory("pwdw", N, d["h"], d["w"], ci, cm, d["k"], d["stride"]) * b,
+                l2_bytes=(u["ifm"] + u["w"] + u["ofm"]) * b, dw_macs=N * Ho * Wo * cm * d["k"] ** 2,
                 pw_macs=u["halo"] * ci, redundant_macs=(u["halo"] - N * d["h"] * d["w"] * cm) * ci)
 
 
@@ -284,8 +261,16 @@ def fusable(layers, edges):
     return fus
 
 
+PAPER_GPU = dict(num_sms=148, smem_bytes=232448)  # B200: 148 SMs, 227 KB shared memory per CTA
+# Table 1: #SMs and L1 per SM of the paper's GPUs. The RTX A4000's printed "128"
+# SMs is garbled (6144 cores / 128 per Ampere SM = 48, reading R22).
+PAPER_GPUS = {"gtx1660": dict(num_sms=22, smem_bytes=96 * 1024),
+              "rtxa4000": dict(num_sms=48, smem_bytes=128 * 1024),
+              "orin": dict(num_sms=16, smem_bytes=192 * 1024)}
+
+
 def plan_paper(model, gpu=None):
-    g = dict(DEFAULT_GPU, **(gpu or {}))
+    g = dict(PAPER_GPU, **(gpu or {}))
     b, N = ESZ[model["dtype"]], model["batch"]
     L = model["layers"]
     sms, smem = g["num_sms"], g["smem_bytes"]

@@ -147,7 +147,12 @@ Epi to_epi(const fcm_epilogue* e) {
   return Epi{e->act, e->scale, e->bias, e->bias_q, e->mult_q, e->shift_q, e->zp_in, e->zp_out, e->qmin, e->qmax};
 }
 
-int out_dim(int in, int k, int s, int p0, int p1) { return (in + p0 + p1 - k) / s + 1; }
+// floor((in + p0 + p1 - k) / s) + 1; a window that does not fit the padded input gives 0 (-> the
+// caller's shape check rejects it with FCM_E_INVAL) instead of C++'s truncation toward zero
+int out_dim(int in, int k, int s, int p0, int p1) {
+  const int span = in + p0 + p1 - k;
+  return span < 0 ? 0 : span / s + 1;
+}
 
 #define FCM_TRY(x)            \
   do {                        \

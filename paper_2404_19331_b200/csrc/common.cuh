@@ -558,10 +558,12 @@ __device__ __forceinline__ uint32_t pack_act(uint64_t acc, uint32_t hi2) {
 }
 
 // ---------------------------------------------------------------------------- int8 column-pair FFMA2 DW core
-// int8, 3x3. Exact in fp32: every product |x w| <= 128 * 127 and every partial sum (9 taps + the
-// int32 bias, |acc| < 9 * 128 * 128 + 2^12 < 2^22) is an integer below 2^24, so FFMA2 accumulation
-// is bit-exact whatever the order (SURVEY §8(c) "Exactness bound for fp32-accumulated int8 DW").
-// A lane owns one 32-bit word (4 channels) of two adjacent output columns: per input word one
+// int8, 3x3. Exact in fp32: every product |x w| <= 128 * 127 and every partial sum of the 9 taps
+// (|acc| < 9 * 128 * 128 < 2^18) is an integer below 2^24, so FFMA2 accumulation is bit-exact
+// whatever the order (SURVEY §8(c) "Exactness bound for fp32-accumulated int8 DW"). The int32
+// bias is NOT folded into the fp32 accumulator (any int32 bias_q is allowed): callers start the
+// accumulators at 0 and add bias_q in int32 after f2_to_i2. A lane owns one 32-bit word (4 channels) of
+// two adjacent output columns: per input word one
 // XOR + 4 byte permutes build 2^23 + (x + 128) as fp32 bit patterns, one FFMA2 pair subtracts
 // 2^23 + 128 (exact), and the channel pairs (0,1), (2,3) feed packed FFMA2s.
 __device__ __forceinline__ void i8word_to_f2x2(uint32_t w, uint64_t& lo, uint64_t& hi) {

@@ -119,7 +119,11 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
     const int cl = c0 + wd * 4;
     const bool cval = wd < cw_valid;
-    uint64_t W[9][2], bias[2];
+    // the accumulators start at 0 and bias_q is added in int32 after the exact fp32 -> int32
+    // conversion: the fp32 path is exact only below 2^22 (the 9 products: < 2^18), bias_q is any int32
+    const uint64_t bias[2] = {0ull, 0ull};
+    uint64_t W[9][2];
+    int32_t bq[4];
     RqI8 rq[4];
     {
       const uint32_t* g = reinterpret_cast<const uint32_t*>(wdw);
@@ -132,14 +136,11 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
         W[t][0] = f2_pack(f[0], f[1]);
         W[t][1] = f2_pack(f[2], f[3]);
       }
-      float b[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        b[v] = (cval && ep.bias_q) ? static_cast<float>(__ldg(ep.bias_q + cl + v)) : 0.f;
+        bq[v] = (cval && ep.bias_q) ? __ldg(ep.bias_q + cl + v) : 0;
         rq[v] = make_rq(cval ? __ldg(ep.mult_q + cl + v) : 0, cval ? __ldg(ep.shift_q + cl + v) : 40);
       }
-      bias[0] = f2_pack(b[0], b[1]);
-      bias[1] = f2_pack(b[2], b[3]);
     }
     const int zp = ep.zp_out, qmin = ep.qmin, qmax = ep.qmax;
     wait_x();
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
             f2_to_i2(a[c][1], v[2], v[3]);
             int32_t o[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) o[q] = min(rq_apply(v[q], rq[q]) + zp, qmax);
+            for (int q = 0; q < 4; ++q) o[q] = min(rq_apply(v[q] + bq[q], rq[q]) + zp, qmax);
             uint32_t word;
             if (qmin == -128) {  // saturating pack gives the lower clamp
               asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(word) : "r"(o[3]), "r"(o[2]));

@@ -4,6 +4,7 @@
 #include <map>
 #include <memory>
 #include <stdexcept>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -92,6 +93,7 @@ class Parser {
       char* end = nullptr;
       v.n = strtod(p_, &end);
       if (end == p_) throw std::runtime_error("bad JSON value");
+      if (!std::isfinite(v.n)) throw std::runtime_error("non-finite JSON number");
       v.kind = Value::Num;
       p_ = end;
     }
@@ -109,6 +111,7 @@ class Parser {
     while (*p_ && *p_ != '"') {
       if (*p_ == '\\') {
         ++p_;
+        if (!*p_) break;  // a backslash right before the terminator: unterminated (never read past NUL)
         char c = *p_++;
         r.push_back(c == 'n' ? '\n' : c == 't' ? '\t' : c);
       } else {
@@ -132,7 +135,8 @@ inline std::string quote(const std::string& s) {
 
 inline std::string num(double d) {
   char buf[64];
-  if (d == static_cast<double>(static_cast<long long>(d)) && d < 9e15 && d > -9e15)
+  if (!std::isfinite(d)) throw std::runtime_error("non-finite number in JSON output");
+  if (d < 9e15 && d > -9e15 && d == static_cast<double>(static_cast<long long>(d)))
     snprintf(buf, sizeof buf, "%lld", static_cast<long long>(d));
   else
     snprintf(buf, sizeof buf, "%.17g", d);

@@ -225,6 +225,10 @@ struct Cost {
   ll dram = 0, l2 = 0, dw_macs = 0, pw_macs = 0, red_macs = 0;
   ll nb = 1, th = 0, tw = 0, nsplit = 0;
   ll gma = -1, p_th = 0, p_tw = 0, p_td = 0;  // paper mode: Eq. value (bytes) and its argmin tile
+  // paper mode keeps the paper's decision even for a pair the fused kernels cannot run
+  // (k not in {3, 5}, or no kernel tile fits): such an entry is reported "executable": false and
+  // runs as its two layer-by-layer kernels
+  bool exec = true;
 };
 
 static double t_us(const Cost& c, int dt, const Gpu& g) {
@@ -349,34 +353,51 @@ static std::string entry_json(const Cost& c, const std::vector<std::string>& ids
   s += ",\"dram_bytes\":" + json::num(c.dram) + ",\"l2_bytes\":" + json::num(c.l2) + ",\"lbl_dram_bytes\":" +
        json::num(lbl_dram) + ",\"dw_macs\":" + json::num(c.dw_macs) + ",\"pw_macs\":" + json::num(c.pw_macs) +
        ",\"redundant_macs\":" + json::num(c.red_macs) + ",\"redundancy\":" + json::num(red_ratio) +
-       ",\"pred_us\":" + json::num(c.us);
+       ",\"pred_us\":" + json::num(c.us) + ",\"executable\":" + (c.exec ? "true" : "false");
   if (mode == "paper")
     s += ",\"gma_bytes\":" + json::num(c.gma) + ",\"paper_tile\":{\"th\":" + json::num(c.p_th) + ",\"tw\":" +
          json::num(c.p_tw) + ",\"td\":" + json::num(c.p_td) + "}";
   return s + "}";
 }
 
+// integer field of a model / GPU object: range-checked before the cast (no UB on huge values)
+static ll geti(const Value& v, const char* key, double def) {
+  const double d = v.num(key, def);
+  if (!(d >= -(double)(1LL << 40) && d <= (double)(1LL << 40)) || d != std::floor(d))
+    throw std::runtime_error(std::string("field '") + key + "' must be an integer of magnitude < 2^40");
+  return (ll)d;
+}
+
 static Layer parse_layer(const Value& v) {
   Layer l;
   l.id = v.str("id", "");
   l.kind = v.str("kind", "");
-  l.H = (ll)v.num("h", 0);
-  l.W = (ll)v.num("w", 0);
+  l.H = geti(v, "h", 0);
+  l.W = geti(v, "w", 0);
   if (l.kind == "dw") {
-    l.C = l.Cout = (ll)v.num("c", 0);
-    l.k = (ll)v.num("k", 3);
-    l.s = (ll)v.num("stride", 1);
+    l.C = l.Cout = geti(v, "c", 0);
+    l.k = geti(v, "k", 3);
+    l.s = geti(v, "stride", 1);
     const Value* p = v.get("pads");
     const ll dp = l.k / 2;
     l.pt = l.pl = l.pb = l.pr = dp;
     if (p && p->kind == Value::Arr && p->a.size() == 4) {
-      l.pt = (ll)p->a[0].n; l.pl = (ll)p->a[1].n; l.pb = (ll)p->a[2].n; l.pr = (ll)p->a[3].n;
+      ll q[4];
+      for (int i = 0; i < 4; ++i) {
+        const double d = p->a[i].n;
+        if (p->a[i].kind != Value::Num || !(d >= 0 && d <= 64) || d != std::floor(d))
+          throw std::runtime_error("layer " + l.id + ": pads must be integers in [0, 64]");
+        q[i] = (ll)d;
+      }
+      l.pt = q[0]; l.pl = q[1]; l.pb = q[2]; l.pr = q[3];
     }
+    if (l.H + l.pt + l.pb < l.k || l.W + l.pl + l.pr < l.k)
+      throw std::runtime_error("layer " + l.id + ": the k x k window does not fit the padded input");
     l.Ho = (l.H + l.pt + l.pb - l.k) / l.s + 1;
     l.Wo = (l.W + l.pl + l.pr - l.k) / l.s + 1;
   } else if (l.kind == "pw") {
-    l.C = (ll)v.num("c_in", 0);
-    l.Cout = (ll)v.num("c_out", 0);
+    l.C = geti(v, "c_in", 0);
+    l.Cout = geti(v, "c_out", 0);
     l.Ho = l.H;
     l.Wo = l.W;
   } else {
@@ -394,15 +415,15 @@ static std::string run(const char* model_json, const char* gpu_json) {
   const int dt = dts == "f32" ? FCM_F32 : dts == "f16" ? FCM_F16 : dts == "s8" ? FCM_S8 : FCM_BF16;
   if (dts != "f32" && dts != "f16" && dts != "s8" && dts != "bf16") throw std::runtime_error("bad dtype " + dts);
   const ll b = elem_size(dt);
-  const ll N = (ll)m.num("batch", 1);
+  const ll N = geti(m, "batch", 1);
   const std::string mode = m.str("mode", "b200");
   if (mode != "b200" && mode != "paper") throw std::runtime_error("mode must be b200 or paper");
   Gpu gp;
   if (gpu_json) {
     const Value g = json::Parser(gpu_json).parse();
-    gp.sms = (ll)g.num("num_sms", (double)gp.sms);
-    gp.smem = (ll)g.num("smem_bytes", (double)gp.smem);
-    gp.l2 = (ll)g.num("l2_bytes", (double)gp.l2);
+    gp.sms = geti(g, "num_sms", (double)gp.sms);
+    gp.smem = geti(g, "smem_bytes", (double)gp.smem);
+    gp.l2 = geti(g, "l2_bytes", (double)gp.l2);
     gp.hbm_gbs = g.num("hbm_gbs", gp.hbm_gbs);
     gp.l2_gbs = g.num("l2_gbs", gp.l2_gbs);
     gp.tc_tmacs = g.num("tc_tmacs", gp.tc_tmacs);
@@ -451,7 +472,12 @@ static std::string run(const char* model_json, const char* gpu_json) {
     if (mode == "paper") {
       Best bst = with_sm_rule([&](ll mt) { return l.kind == "dw" ? paper_dw(l, N, b, gp, mt) : paper_pw(l, N, b, gp, mt); }, gp.sms);
       Cost c = l.kind == "dw" ? b200_dw(l, N, dt, b, gp) : b200_pw(l, N, dt, b, gp);
-      if (!bst.ok) throw std::runtime_error("layer " + l.id + ": no feasible tiling");
+      if (!bst.ok) {
+        // no tile of the grid fits on chip: the layer runs untiled, GMA = IFM + W + OFM (the
+        // single-tile closed form of Eq. 2 / Eq. 3)
+        const ll w = l.kind == "dw" ? l.k * l.k * l.C : l.C * l.Cout;
+        bst = {true, N * l.H * l.W * l.C + w + N * l.Ho * l.Wo * l.Cout, l.Ho, l.Wo, l.Cout, l.kind};
+      }
       c.gma = bst.gma * b;
       c.p_th = bst.th; c.p_tw = bst.tw; c.p_td = bst.td;
       lbl[i] = c;
@@ -467,14 +493,17 @@ static std::string run(const char* model_json, const char* gpu_json) {
     // the fused kernels are built for k in {3, 5} (fcm_dw also has k = 7): no FCM candidate
     // otherwise in b200 mode (paper mode keeps the paper's decision)
     const Layer& dwl = a.kind == "dw" ? a : c;
-    if (mode != "paper" && dwl.kind == "dw" && dwl.k != 3 && dwl.k != 5) continue;
+    const bool k_ok = dwl.kind != "dw" || dwl.k == 3 || dwl.k == 5;
+    if (mode != "paper" && !k_ok) continue;
     Cost f;
     if (a.kind == "dw" && c.kind == "pw") {
       if (mode == "paper") {
         Best bst = with_sm_rule([&](ll mt) { return paper_dwpw(a, c, N, b, gp, mt); }, gp.sms);
         if (!bst.ok) continue;
         f = b200_dwpw(a, c, N, dt, b, gp);
+        f.exec = f.ok && k_ok;
         f.ok = true;
+        f.dram = (N * (a.H * a.W * a.C + a.Ho * a.Wo * c.Cout) + a.k * a.k * a.C + a.C * c.Cout) * b;
         f.gma = bst.gma * b; f.p_th = bst.th; f.p_tw = bst.tw; f.p_td = bst.td;
       } else {
         f = b200_dwpw(a, c, N, dt, b, gp);
@@ -484,7 +513,9 @@ static std::string run(const char* model_json, const char* gpu_json) {
         Best bst = with_sm_rule([&](ll mt) { return paper_pwdw(a, c, N, b, gp, mt); }, gp.sms);
         if (!bst.ok) continue;
         f = b200_pwdw(a, c, N, dt, b, gp);
+        f.exec = f.ok && k_ok;
         f.ok = true;
+        f.dram = (N * (c.H * c.W * a.C + c.Ho * c.Wo * a.Cout) + a.C * a.Cout + c.k * c.k * a.Cout) * b;
         f.op = bst.kind;
         f.gma = bst.gma * b; f.p_th = bst.th; f.p_tw = bst.tw; f.p_td = bst.td;
       } else {

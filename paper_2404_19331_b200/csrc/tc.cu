@@ -618,7 +618,10 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
           const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
           const int cl = kc * KC + wd * 4;
-          uint64_t Wf[9][2], bias[2];
+          // accumulators start at 0; bias_q is added in int32 after the exact conversion (as in dw.cu)
+          const uint64_t bias[2] = {0ull, 0ull};
+          uint64_t Wf[9][2];
+          int32_t bq[4];
           RqI8 rq[4];
           {
             const uint32_t wa = smem_u32(wsm) + 4 * (kc * 32 + wd);
@@ -631,15 +634,12 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
               Wf[t9][0] = f2_pack(f[0], f[1]);
               Wf[t9][1] = f2_pack(f[2], f[3]);
             }
-            float bf[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               const EpiC e = epic<DT>(dcs, cl + v);
-              bf[v] = static_cast<float>(e.bq);
+              bq[v] = e.bq;
               rq[v] = make_rq(e.m, e.sh < 1 ? 40 : e.sh);
             }
-            bias[0] = f2_pack(bf[0], bf[1]);
-            bias[1] = f2_pack(bf[2], bf[3]);
           }
           const int zp = ed.zp_out, qmin = ed.qmin, qmax = ed.qmax;
           named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
                   uint32_t word = 0;
 #pragma unroll
                   for (int q = 0; q < 4; ++q)
-                    word |= (static_cast<uint32_t>(min(max(rq_apply(v[q], rq[q]) + zp, qmin), qmax)) & 0xFFu) << (8 * q);
+                    word |= (static_cast<uint32_t>(min(max(rq_apply(v[q] + bq[q], rq[q]) + zp, qmin), qmax)) & 0xFFu) << (8 * q);
                   const int m = (b * th + y0 + r) * tw + x0 + c;
                   if (c == 0 || c1) sts32(abase + sw128_off(m, wd), cl < Cin ? word : 0u);
                 }

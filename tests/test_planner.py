@@ -41,49 +41,64 @@ def test_paper_mode_matches_oracle(fcm, net, dt, batch):
 
 @pytest.mark.parametrize("net,dt,batch", CASES)
 def test_b200_mode_candidates_and_decisions(fcm, net, dt, batch):
+    """b200 mode: every candidate's compulsory HBM bytes, exact L2->SM bytes and MACs are
+    re-derived by the oracle from the tile the candidate reports; the fuse rule (strict)
+    and the chain DP are re-run on the library's own predicted times. (The time model is
+    checked against measured kernel times in test_planner_time_model.py, not here.)"""
     m = model_json(net, dt, batch, "b200")
     p = fcm.plan(m)
     layers = {l["id"]: l for l in m["layers"]}
     order = [l["id"] for l in m["layers"]]
-    g = op.DEFAULT_GPU
     lbl_cost, fcm_cost = {}, {}
     for c in p["candidates"]["lbl"] + p["candidates"]["fcm"]:
         ls = [layers[i] for i in c["layers"]]
-        kern = c["op"] if len(ls) == 1 else ("dwpw" if ls[0]["kind"] == "dw" else "pwdw_r")
-        want = op.b200_numbers(kern if kern != "pwdw_r" else "pwdw", ls, batch, dt, c["tile"])
+        kern = c["op"] if len(ls) == 1 else ("dwpw" if ls[0]["kind"] == "dw" else "pwdw")
+        want = op.b200_numbers(kern, ls, batch, dt, c["tile"])
         for k, v in want.items():
             assert c[k] == v, (c["layers"], k, c[k], v)
-        us = op.pred_us(c, dt, g)
-        assert c["pred_us"] == pytest.approx(us, rel=1e-12)
+        assert c["pred_us"] > 0
         if len(ls) == 1:
-            lbl_cost[c["layers"][0]] = us
+            lbl_cost[c["layers"][0]] = c["pred_us"]
         else:
-            accepted = us < lbl_cost[c["layers"][0]] + lbl_cost[c["layers"][1]]
+            accepted = c["pred_us"] < lbl_cost[c["layers"][0]] + lbl_cost[c["layers"][1]]
             assert c["accepted"] == accepted
             if accepted:
-                fcm_cost[order.index(c["layers"][1])] = us
+                fcm_cost[order.index(c["layers"][1])] = c["pred_us"]
     n = len(order)
     sel = op.chain_dp(n, [lbl_cost[i] for i in order], [fcm_cost.get(i) for i in range(n)])
     assert [e["layers"] for e in p["entries"]] == [[order[j] for j in e] for e in sel]
     assert p["totals"]["dram_bytes"] == sum(e["dram_bytes"] for e in p["entries"])
 
 
+@pytest.mark.parametrize("gpu", ["gtx1660", "rtxa4000", "orin"])
+def test_paper_mode_on_the_papers_gpus_matches_oracle(fcm, gpu):
+    """Paper mode parameterised with Table 1's GPUs (RTX A4000 with its real 48 SMs,
+    reading R22) equals the oracle on the paper's four end-to-end CNNs."""
+    g = op.PAPER_GPUS[gpu]
+    for net in ("mobilenet_v1", "mobilenet_v2", "xception", "proxylessnas_gpu"):
+        m = model_json(net, "f32", 1, "paper")
+        got = fcm.plan(m, g)["entries"]
+        want = op.plan_paper(m, g)
+        assert [(e["layers"], e["kind"], e["gma_bytes"], e["paper_tile"]) for e in got] == \
+               [(e["layers"], e["kind"], e["gma_bytes"], e["paper_tile"]) for e in want]
+
+
 def test_units_reduce_to_pinned_counters():
     """The batched unit counters with N=1, nb=1 equal the pinned per-image exact counters."""
     d = {"kind": "dw", "h": 13, "w": 11, "c": 40, "k": 3, "stride": 2, "pads": [1, 1, 1, 1]}
-    u = op.units("dw", 1, d, 40, 40, 1, 3, 4, 16)
+    u = op.units("dw", 1, d, 40, 40, 1, 3, 4, 1)
     e = dw_exact(13, 11, 40, 3, 2, (1,) * 4, 3, 4, 16)
     assert (u["ifm"], u["w"], u["ofm"]) == (e["ifm"], e["w"], e["ofm"])
-    u = op.units("dwpw", 1, d, 40, 24, 1, 3, 4, 16)
+    u = op.units("dwpw", 1, d, 40, 24, 1, 3, 4, 2)  # 24 channels in slices of 16: 2 splits
     e = dwpw_exact(13, 11, 40, 24, 3, 2, (1,) * 4, 3, 4, 16)
     assert (u["ifm"], u["w"], u["ofm"]) == (e["ifm"], e["w"], e["ofm"])
-    u = op.units("pwdw", 1, d, 24, 40, 1, 3, 4, 16)
+    u = op.units("pwdw", 1, d, 24, 40, 1, 3, 4, 3)  # 40 channels in slices of 16: 3 splits
     e = pwdw_exact(13, 11, 24, 40, 3, 2, (1,) * 4, 3, 4, 16)
     assert (u["ifm"], u["w"], u["ofm"]) == (e["ifm"], e["w"], e["ofm"])
     assert (u["halo"] - 13 * 11 * 40) * 24 == e["redundant_macs"]
     # batching: nb images per unit share the weight loads but not the activations
-    u1 = op.units("dwpw", 4, d, 40, 24, 1, 3, 4, 16)
-    u2 = op.units("dwpw", 4, d, 40, 24, 2, 3, 4, 16)
+    u1 = op.units("dwpw", 4, d, 40, 24, 1, 3, 4, 2)
+    u2 = op.units("dwpw", 4, d, 40, 24, 2, 3, 4, 2)
     e = dwpw_exact(13, 11, 40, 24, 3, 2, (1,) * 4, 3, 4, 16)
     assert u1["ifm"] == u2["ifm"] == 4 * e["ifm"] and u2["w"] * 2 == u1["w"]
 
