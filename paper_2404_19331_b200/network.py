@@ -94,11 +94,21 @@ class Network:
             return (self.batch, ho, wo, l["c"])
         return (self.batch, l["h"], l["w"], l["c_out"])
 
+    def _entries(self):
+        """Plan entries as launched: a paper-mode FCM entry the fused kernels cannot run
+        ("executable": false -- k outside {3, 5} or no kernel tile) runs as its LBL layers."""
+        for e in self.plan["entries"]:
+            if e.get("executable", True) or len(e["layers"]) == 1:
+                yield e
+            else:
+                for lid in e["layers"]:
+                    yield {"op": self.layers[lid]["kind"], "kind": self.layers[lid]["kind"], "layers": [lid]}
+
     def _build_steps(self):
         cur = self.x
         stage_in = {}
-        self.outputs = []
-        for e in self.plan["entries"]:
+        self.outputs, self.inputs, self.entries = [], [], []
+        for e in self._entries():
             lids = e["layers"]
             l0 = self.layers[lids[0]]
             bi = l0["block"]
@@ -117,6 +127,8 @@ class Network:
             self.step_info.append(dict(e, in_shape=tuple(src.shape), out_shape=tuple(out.shape)))
             cur = out
             self.outputs.append(out)
+            self.inputs.append(src)
+            self.entries.append(e)
         self.out = cur
 
     def _make_call(self, e, src, out):

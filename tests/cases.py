@@ -160,3 +160,29 @@ class Case:
     def check(self, dev="cuda:0"):
         ref, mag = self.oracle()
         return compare(self.gpu(dev), ref, mag, self.fmt, f"{self.op}/{self.fmt}")
+
+
+def oracle_entry(e, layers, prm, x, fmt):
+    """Oracle output (and R10 magnitude, None for int8) of one plan entry applied to input x."""
+    op, lids = e["op"], e["layers"]
+    pads = lambda l: (l["k"] // 2,) * 4
+    f64 = fmt != "s8"
+    if op == "dw":
+        l, p = layers[lids[0]], prm[lids[0]]
+        ref = oc.dw(x, p["w"], l["stride"], pads(l), p, fmt)
+        return ref, (oc.mag_dw(x, p["w"], l["stride"], pads(l), p) if f64 else None)
+    if op == "pw":
+        p = prm[lids[0]]
+        return oc.pw(x, p["w"], p, fmt), (oc.mag_pw(x, p["w"], p) if f64 else None)
+    if op == "dwpw":
+        l, pd, pp = layers[lids[0]], prm[lids[0]], prm[lids[1]]
+        ref = oc.dwpw(x, pd["w"], l["stride"], pads(l), pd, pp["w"], pp, fmt)
+        return ref, (oc.mag_dwpw(x, pd["w"], l["stride"], pads(l), pd, pp["w"], pp) if f64 else None)
+    if op == "pwdw_r":
+        l, pp, pd = layers[lids[1]], prm[lids[0]], prm[lids[1]]
+        ref = oc.pwdw(x, pp["w"], pp, pd["w"], l["stride"], pads(l), pd, fmt)
+        return ref, (oc.mag_pwdw(x, pp["w"], pp, pd["w"], l["stride"], pads(l), pd) if f64 else None)
+    if op == "pwpw":
+        p1, p2 = prm[lids[0]], prm[lids[1]]
+        return oc.pwpw(x, p1["w"], p1, p2["w"], p2, fmt), (oc.mag_pwpw(x, p1["w"], p1, p2["w"], p2) if f64 else None)
+    raise ValueError(op)

@@ -8,6 +8,7 @@ import pytest
 import synth
 import torch
 
+from oracle import conv as oc
 from tests.cases import Case, as_np, compare, stored
 
 pytestmark = pytest.mark.gpu
@@ -244,3 +245,26 @@ def test_dw_cp_async_staging_unaligned_pitch(fmt, c, k, s):
     and past C; the cores are unchanged (int8 bit-exact, floats within tolerance)."""
     Case("dw", fmt, 2, 11, 13, c, k=k, s=s).check()
     Case("dw", fmt, 1, 9, 10, c, k=k, s=s, tile={"tile_h": 3, "tile_w": 5}).check()
+
+
+@pytest.mark.parametrize("op", ["dw", "dwpw"])
+@pytest.mark.parametrize("s", [1, 2])
+@pytest.mark.parametrize("shift", [47, 48])
+def test_int8_dw_large_bias_q(op, s, shift):
+    """int8 DW with |bias_q| in [1, 2) x 2^22 .. 2^23 (any int32 is legal, fcm.h): the FFMA2 DW
+    cores accumulate the taps exactly in fp32 (|sum| < 2^18) and add bias_q in int32 afterwards.
+    Shifts 47 / 48 (scale ~2^-17 / 2^-18) keep the outputs unsaturated with zp_out = 0, so a bias
+    folded into the fp32 accumulator (exact int conversion only below 2^22) would show. Bit-exact."""
+    import numpy as np
+    c = Case(op, "s8", 2, 19, 23, 96, 48, k=3, s=s, act_dw=synth.ACT_NONE) if op == "dwpw" else \
+        Case(op, "s8", 2, 19, 23, 96, k=3, s=s, act_dw=synth.ACT_NONE)
+    p = c.pd
+    rng = np.random.default_rng(shift)
+    nc = len(p["bias_q"])
+    mag = rng.integers(1 << 22, 1 << (shift - 24), size=nc)
+    p["bias_q"] = (mag * rng.choice([-1, 1], size=nc)).astype(np.int64)
+    p["shift_q"] = np.full(nc, shift, dtype=np.int64)
+    p["zp_out"], p["qmin"], p["qmax"] = 0, -128, 127
+    t = oc.dw(as_np(c.x, "s8"), p["w"], s, c.pads, p, "s8")
+    assert (np.abs(t) < 127).mean() > 0.9 and (np.abs(t) > 8).mean() > 0.5  # unsaturated, bias-driven
+    c.check()

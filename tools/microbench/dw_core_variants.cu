@@ -61,7 +61,7 @@ __global__ void k(const __grid_constant__ WP wp, int iters, uint32_t* out) {
     const uint64_t bias = f2_pack(0.5f + lf, 0.25f - lf);
     // X tile [rows 20][cols 40][32 words]
     for (int it = 0; it < iters; ++it) {
-      const int x0 = (V == 0 ? 2 : 4) * ((warp + it) & 7), y0 = ((warp >> 3) + it) & 1;
+      const int x0 = (V == 0 ? 2 : 4) * ((warp + it) & 7), y0 = SEG > 8 ? 0 : ((warp >> 3) + it) & 1;
       const uint32_t src = xt + ((y0 * 40 + x0) * 32 + lane) * 4;
       const uint32_t a0 = ab + (lane >> 2) * kAlbo + (lane & 3) * 4 + (uint32_t)(y0 * 32 + x0) * 16;
       if constexpr (V == 0) {
@@ -144,6 +144,8 @@ int main() {
   };
   for (int nw : {8, 12, 16}) {
     run(k<0, 8>, "V0 pair (lane=word, 2 col), SEG 8", nw, 2 * 8 * 64);
+    run(k<0, 14>, "V0 pair (lane=word, 2 col), SEG 14", nw, 2 * 14 * 64);
+    run(k<0, 4>, "V0 pair (lane=word, 2 col), SEG 4", nw, 2 * 4 * 64);
     run(k<1, 4>, "V1 quad (lane=word, 4 col), SEG 4", nw, 4 * 4 * 64);
     run(k<1, 6>, "V1 quad (lane=word, 4 col), SEG 6", nw, 4 * 6 * 64);
     run(k<1, 8>, "V1 quad (lane=word, 4 col), SEG 8", nw, 4 * 8 * 64);
