@@ -128,42 +128,100 @@ def kernel_family(op):
             "pwpw": "pwpw_tc_kernel"}[op]
 
 
-def per_entry_times(netw, reps=20):
-    """Device time of every plan entry (one kernel each), CUDA events on the launching stream."""
+def per_entry_times(netw, reps=100):
+    """Device time of every plan entry (one kernel each), SURVEY §8(d) protocol: before every
+    timed launch a buffer of 2x the L2 size is written (outside the CUDA-event pair), so each launch
+    starts L2-cold; `reps` launches per entry; median / p10 / p90 in microseconds."""
     st = torch.cuda.current_stream()
-    times = []
+    l2 = torch.cuda.get_device_properties(st.device).L2_cache_size
+    flush = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device=st.device)
+    out = []
     for f in netw.steps:
         for _ in range(2):
             f()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
         torch.cuda.synchronize()
-        ev[0].record(st)
-        for _ in range(reps):
+        for a, b in ev:
+            flush.zero_()
+            a.record(st)
             f()
-        ev[1].record(st)
+            b.record(st)
         torch.cuda.synchronize()
-        times.append(ev[0].elapsed_time(ev[1]) * 1e3 / reps)  # us
-    return times
+        us = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
+        q = lambda p: us[min(len(us) - 1, int(p * (len(us) - 1) + 0.5))]
+        out.append({"median": statistics.median(us), "p10": q(0.1), "p90": q(0.9), "reps": reps})
+    del flush
+    return out
+
+
+def in_step_entry_times(netw, replays=20):
+    """Device time of every plan entry INSIDE the step: the whole stack is captured once more with
+    a pair of CUDA events (graph event-record nodes) around every launch, and this graph is
+    replayed `replays` times; per entry the median over replays of its event pair, in
+    microseconds. Inputs / L2 state are those of the real step (each layer reads what the
+    previous one just wrote); the event nodes serialise neighbouring launches (no PDL overlap)."""
+    st = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+          for _ in netw.steps]
+    s = torch.cuda.Stream()
+    s.wait_stream(st)
+    with torch.cuda.stream(s):
+        netw.run()
+    st.wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for (a, b), f in zip(ev, netw.steps):
+            a.record()
+            f()
+            b.record()
+    samples = [[] for _ in netw.steps]
+    for r in range(replays + 2):
+        g.replay()
+        torch.cuda.synchronize()
+        if r >= 2:
+            for i, (a, b) in enumerate(ev):
+                samples[i].append(a.elapsed_time(b) * 1e3)
+    return [statistics.median(x) for x in samples]
+
+
+def host_cpu():
+    """nproc and the lscpu model name of the host the oracle runs on."""
+    model = None
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
 
 
 def cpu_baseline(net, dtype, seconds=15.0):
     """The oracle (oracle/network.py, numpy fp64 / exact int) as it stands on the host cores,
-    on a bounded sample of the same workload: whole images through the whole stack."""
+    on a bounded sample of the same workload: whole images through the whole stack, timed once
+    with one BLAS thread and once with all cores (the oracle's only parallelism is numpy/BLAS)."""
     from oracle import network as on
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
+    from threadpoolctl import threadpool_info, threadpool_limits
     prm = on.params(net, dtype)
-    t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < seconds:
-        on.forward(net, dtype, n, 1, prm=prm)
-        n += 1
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "images/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n} images x whole {net} DW/PW stack ({dtype}), one at a time, {dt:.1f}s"}
+    on.forward(net, dtype, 0, 1, prm=prm)  # warm-up (allocations, BLAS init)
+
+    def run(limit, secs):
+        with threadpool_limits(limits=limit):
+            threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+            t0, n = time.perf_counter(), 0
+            while time.perf_counter() - t0 < secs:
+                on.forward(net, dtype, n, 1, prm=prm)
+                n += 1
+            return n / (time.perf_counter() - t0), n, threads
+    v1, n1, _ = run(1, seconds / 3)
+    va, na, threads = run(os.cpu_count(), 2 * seconds / 3)
+    cpu = host_cpu()
+    return {"value": va, "unit": "images/s", "cores": threads, "kind": "oracle",
+            "single_thread": {"value": v1, "images": n1}, "host": cpu,
+            "sample": f"{na} (all cores) + {n1} (1 thread) images x whole {net} DW/PW stack ({dtype}), one at a time, "
+                      f"{seconds:.0f} s total"}
 
 
 def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5, energy_gpu=None):
@@ -315,6 +373,12 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     ws, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without torchrun: spawn the N ranks ourselves
+        from paper_2404_19331_b200.replicas import relaunch_under_torchrun
+        relaunch_under_torchrun(args.gpus, [os.path.abspath(__file__)] + sys.argv[1:])
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
     if args.impl == "reference":
         return run_reference(args, ws, rank)
 
@@ -325,24 +389,25 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     import paper_2404_19331_b200 as fcm
     from paper_2404_19331_b200.network import Network, model_json
+    from paper_2404_19331_b200 import replicas
 
+    n0, _ = replicas.shard(args.batch, ws, rank)
+    plan_verify = None
     if args.plan == "measured" and args.mode == "b200":
         # rank 0 measures; every rank executes the same plan (so the shards are bit-identical to
         # a one-GPU run of the same plan and the post-timing verification is meaningful)
         plan = None
         if rank == 0:
-            from paper_2404_19331_b200.autotune import refine
+            from paper_2404_19331_b200.autotune import refine, verify_against_lbl
             plan = refine(args.net, args.dtype, args.batch, device=dev)
-        if ws > 1:
-            box = [plan]
-            torch.distributed.broadcast_object_list(box, src=0)
-            plan = box[0]
+            plan_verify = verify_against_lbl(args.net, args.dtype, plan, device=dev)
+        plan = replicas.broadcast_plan(plan, ws)
     else:
         plan = fcm.plan(model_json(args.net, args.dtype, args.batch, args.mode))
     if args.plan_out and rank == 0:
         with open(args.plan_out, "w") as f:
             json.dump(plan, f, indent=1)
-    netw = Network(args.net, args.dtype, args.batch, plan, device=dev, n0=rank * args.batch)
+    netw = Network(args.net, args.dtype, args.batch, plan, device=dev, n0=n0)
     if args.no_graph:
         netw.run()
         torch.cuda.synchronize()
@@ -387,7 +452,7 @@ def main():
     # H2D copy of step k+1 and the D2H copy of step k-1 run on copy streams while step k computes.
     x_host = netw.x.cpu().pin_memory()
     y_host = [torch.empty(netw.out.shape, dtype=netw.out.dtype).pin_memory() for _ in range(2)]
-    nets = [netw, Network(args.net, args.dtype, args.batch, plan, device=dev, n0=rank * args.batch)]
+    nets = [netw, Network(args.net, args.dtype, args.batch, plan, device=dev, n0=n0)]
     graphs = [graph, (nets[1].capture() if not args.no_graph else _Eager2(nets[1]))]
     cin, cout = torch.cuda.Stream(), torch.cuda.Stream()
     in_ready = [torch.cuda.Event() for _ in range(2)]
@@ -429,26 +494,18 @@ def main():
     e2e_same = bool(torch.equal(y_host[0], y_host[1]))  # both buffer sets ran the same batch and plan
 
     # ---------------- per-entry (per-kernel) device times
-    times_us = per_entry_times(netw)
+    entry_stats = per_entry_times(netw)          # isolated launches, L2-cold, 100 reps each
+    times_us = in_step_entry_times(netw)         # the same launches inside the step (roofline)
 
+    t_ms, t_e2e = replicas.max_over_ranks([t_ms, t_e2e], dev, ws)
     if ws > 1:
-        t = torch.tensor([t_ms, t_e2e], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_ms, t_e2e = float(t[0]), float(t[1])
-        # verification only (after timing): gather per-image checksums over NCCL; rank 0
-        # recomputes the first images of every shard itself -- batch shards are independent,
-        # so the results must be bit-identical
-        ck = netw.out.double().reshape(args.batch, -1).sum(1)
-        allck = [torch.empty_like(ck) for _ in range(ws)]
-        torch.distributed.all_gather(allck, ck)
-        verify = {"gathered_images": ws * args.batch, "checked": 0, "bit_identical": True}
-        if rank == 0:
-            for r in range(ws):
-                probe = Network(args.net, args.dtype, 2, plan, device=dev, n0=r * args.batch)
-                probe.run()
-                mine = probe.out.double().reshape(2, -1).sum(1)
-                verify["checked"] += 2
-                verify["bit_identical"] &= bool(torch.equal(mine, allck[r][:2]))
+        # verification only (after timing): per-image checksums over NCCL; rank 0 recomputes the
+        # first images of every shard with its own Network instance
+        def run_probe(p0, n):
+            probe = Network(args.net, args.dtype, n, plan, device=dev, n0=p0)
+            probe.run()
+            return probe.out
+        verify = replicas.verify_shards(netw.out, args.batch, ws, rank, run_probe)
 
     pk = peaks()
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
@@ -460,7 +517,7 @@ def main():
     sm_hz = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
     dw_mac_s = 148 * 128 * sm_hz
     tc_mac_s = float(pk.get("bf16_tflops", 1598.4)) * 1e12 / 2 * {"s8": 2.0, "f32": 0.5}.get(args.dtype, 1.0)
-    for info, us in zip(netw.step_info, times_us):
+    for info, us, es in zip(netw.step_info, times_us, entry_stats):
         k = kernel_family(info["op"])
         f = fam.setdefault(k, {"us": 0.0, "bytes": 0, "n": 0, "bind_us": 0.0, "t": {"hbm": 0.0, "dw_alu": 0.0, "pw_tc": 0.0}})
         f["us"] += us
@@ -473,6 +530,7 @@ def main():
         for kk in t:
             f["t"][kk] += t[kk]
         rows.append({"op": info["op"], "layers": info["layers"], "tile": info.get("tile"), "us": round(us, 3),
+                     "cold_us": round(es["median"], 3), "cold_p10": round(es["p10"], 3), "cold_p90": round(es["p90"], 3),
                      "dram_bytes": info["dram_bytes"], "l2_bytes": info["l2_bytes"],
                      "lbl_dram_bytes": info["lbl_dram_bytes"],
                      "gbs": round(info["dram_bytes"] / us / 1e3, 1), "frac_hbm": round(info["dram_bytes"] / us / 1e3 / hbm_peak, 3),
@@ -505,6 +563,8 @@ def main():
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                          "traffic": traffic_from_profiles(dom, config_tag),
                          "share_of_step": round(d["us"] / sum_us, 3), "launches_per_step": d["n"],
+                         "timing": "CUDA events around every launch inside the captured step (median of 20 replays); "
+                                   "isolated L2-cold medians (100 launches, 2x L2 flushed before each) in the layers file",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")},
             "binding_roof": {"kernel": dom, "t_us": {kk: round(v, 2) for kk, v in d["t"].items()},
                              "bound": max(d["t"], key=d["t"].get), "measured_us": round(d["us"], 2),
@@ -524,6 +584,8 @@ def main():
             line["energy"] = energy
         if ws > 1:
             line["verify"] = verify
+        if plan_verify is not None:
+            line["plan_verify"] = plan_verify
         if not args.no_cudnn and args.dtype in ("bf16", "f16", "f32"):
             try:
                 cb = cudnn_stack(args.net, args.dtype, args.batch, dev,
@@ -536,14 +598,14 @@ def main():
                     line["cudnn_baseline"] = cb
             except Exception as e:  # baseline only; never fails the bench
                 line["cudnn_baseline"] = {"error": str(e)[:200]}
-        if not args.no_cpu_baseline and ws == 1:
+        if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.net, args.dtype, args.cpu_seconds)
         if args.layers_out:
             with open(args.layers_out, "w") as f:
                 json.dump({"config": config_tag, "rows": rows, "families": fam, "plan_totals": plan["totals"]}, f,
                           indent=1)
         for r in rows:
-            print(f"{r['op']:7s} {','.join(r['layers']):12s} {r['us']:9.2f}us {r['gbs']:8.1f}GB/s "
+            print(f"{r['op']:7s} {','.join(r['layers']):12s} {r['us']:9.2f}us cold {r['cold_us']:.1f} [{r['cold_p10']:.1f},{r['cold_p90']:.1f}] {r['gbs']:8.1f}GB/s "
                   f"frac {r['frac_hbm']:.3f} pred {r['pred_us']:8.2f}us tile {r['tile']}", file=sys.stderr)
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -173,3 +173,22 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
                          fused_pairs=sum(1 for e in entries if len(e["layers"]) == 2))
     out.pop("candidates", None)
     return out
+
+
+def verify_against_lbl(net: str, dtype: str, plan: dict, device="cuda", images: int = 4):
+    """Run the chosen plan once on real (seeded) images and compare it with the all-LBL plan of
+    the same stack: an FCM computes exactly PW(DW(X)) / DW(PW(X)) with T in the FM dtype (P:85,
+    P:111), so int8 must match bit for bit and floats up to the R3b reassociation (rare
+    1-ulp flips of T, far inside the 2e-2 / 1e-5 tolerances)."""
+    lbl = {"entries": fcm.plan(model_json(net, dtype, images))["candidates"]["lbl"]}
+    a = Network(net, dtype, images, {"entries": plan["entries"]}, device=device)
+    a.run()
+    b = Network(net, dtype, images, lbl, device=device)
+    b.run()
+    torch.cuda.synchronize()
+    ya, yb = a.out.float(), b.out.float()
+    same = bool(torch.equal(a.out, b.out))
+    rel = float(((ya - yb).abs().max() / yb.abs().max().clamp_min(1e-30)).item())
+    tol = 0.0 if dtype == "s8" else (1e-5 if dtype == "f32" else 2e-2)
+    return {"images": images, "vs": "all-LBL plan on the GPU", "bit_identical": same,
+            "max_abs_diff_over_max_abs": rel, "ok": bool(torch.isfinite(ya).all()) and (same or rel <= tol)}

@@ -65,3 +65,50 @@ def test_shard_slices_are_exact():
     a = synth.activations(7, "r", 0, 6, 4, 4, 8, "int8")
     b = synth.activations(7, "r", 2, 3, 4, 4, 8, "int8")
     assert np.array_equal(a[2:5], b)
+
+
+def _replica_worker(rank, world, port, per_rank, q):
+    """The replica logic bench.py runs over NCCL (paper_2404_19331_b200/replicas.py), here over
+    gloo: shard, plan broadcast, max-over-ranks timing, checksum all_gather + rank-0 re-check."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2404_19331_b200 import replicas
+    n0, n = replicas.shard(per_rank, world, rank)
+    plan = replicas.broadcast_plan({"entries": ["chosen by rank 0"]} if rank == 0 else None, world)
+    t = replicas.max_over_ranks([1.0 + rank, 5.0 - rank], "cpu", world)
+    out = torch.from_numpy(onet.forward("single_dwpw", "s8", n0, n))
+    run_probe = lambda p0, k: torch.from_numpy(onet.forward("single_dwpw", "s8", p0, k))
+    ok = replicas.verify_shards(out, per_rank, world, rank, run_probe)
+    # a corrupted shard must be caught
+    bad = replicas.verify_shards(out + (1 if rank == 1 else 0), per_rank, world, rank, run_probe)
+    if rank == 0:
+        q.put((plan, t, ok, bad))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_replica_logic_over_gloo():
+    world, per_rank = 2, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, world, port, per_rank, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    plan, t, ok, bad = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert plan == {"entries": ["chosen by rank 0"]}
+    assert t == [2.0, 5.0]
+    assert ok == {"gathered_images": 6, "checked": 4, "bit_identical": True}
+    assert bad["bit_identical"] is False
+
+
+def test_shard_rejects_bad_requests():
+    import pytest
+    from paper_2404_19331_b200 import replicas
+    assert replicas.shard(256, 8, 7) == (1792, 256)
+    with pytest.raises(ValueError):
+        replicas.shard(256, 2, 2)
+
