@@ -15,12 +15,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INC = os.path.join(ROOT, "include")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libfcm.so")
+# development variants: FCM_BUILD_DEFS="-DX=1 ..." builds into build/obj-<tag>, FCM_BUILD_OUT names the .so
+DEFS = os.environ.get("FCM_BUILD_DEFS", "").split()
+OBJ = os.path.join(ROOT, "build", "obj" + ("-" + "".join(c for c in "".join(DEFS) if c.isalnum()) if DEFS else ""))
+LIB = os.environ.get("FCM_BUILD_OUT") or os.path.join(HERE, "libfcm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", INC, "-I", CSRC,
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + DEFS
 
 
 def _deps():

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "fcm.h"
 #include "ptx.cuh"
@@ -538,6 +539,95 @@ __device__ __forceinline__ void dw3_pair(uint32_t src, int col_bytes, int row_by
   }
 }
 
+// ---------------------------------------------------------------------------- column-group FHFMA DW core
+// bf16 / f16, 3x3. Same lane mapping as dw3_pair (a lane owns one 32-bit word = 2 channels of NC
+// adjacent output columns over SEG rows, input rows streamed once), but the taps are the mixed
+// fp32 += bf16 x bf16 FMA (fma.rn.f32.bf16 / .f16, SASS FHFMA with .H0/.H1 half selectors): the
+// packed words feed the FMA directly, so there is no bf16 -> fp32 widening. Measured on B200
+// (tools/microbench/ffma2_operands.cu): every ALU-pipe instruction (PRMT, LOP3, ...) costs about as
+// much issue time as one FFMA2, so the widening (2 PRMT per input word) made up ~40 % of dw3_pair's
+// pipe time. FHFMA does 32 MACs per warp instruction at the FFMA rate (~125 MAC/clk/SM, fma_rates.cu).
+// Products of two bf16 / f16 values are exact in fp32, so each tap is one correctly rounded fp32
+// FMA -- the same arithmetic as widening first. Weights are the raw packed DW weights; the
+// accumulators start at 0 and the caller applies the per-channel scale / bias (R3) in its sink.
+// sink(r, c, acc) gets output row r, column c (compile-time) and the fp32 pair as (lo, hi).
+// `src` addresses the item's first input row (row y0 * S of the staged tile, this lane's word);
+// rows are COLB bytes per pixel apart and `row_bytes` apart. All (SEG - 1) S + 3 input rows must
+// lie inside the staged tile: callers shift a ragged last segment up (y0 = th - SEG) and recompute
+// the overlap instead of clamping row indices, so the row addresses are plain increments.
+template <int DT, int S, int SEG, int NC, int COLB, class Sink>
+__device__ __forceinline__ void dw3_cols_h(uint32_t src, int row_bytes, const uint32_t (&W)[9], Sink&& sink) {
+  constexpr int NCW = (NC - 1) * S + 3;   // input words per row feeding NC output columns
+  constexpr int WR = (SEG - 1) * S + 3;   // input rows of the segment
+  constexpr int PD = 2;                   // rows loaded ahead of their use
+  float acc[SEG][NC][2];
+  uint32_t raw[WR][NCW];
+  auto load_row = [&](int ii) {
+    const uint32_t rp = src + ii * row_bytes;
+#pragma unroll
+    for (int j = 0; j < NCW; ++j) raw[ii][j] = lds32(rp + j * COLB);
+  };
+#pragma unroll
+  for (int ii = 0; ii < PD && ii < WR; ++ii) load_row(ii);
+#pragma unroll
+  for (int ii = 0; ii < WR; ++ii) {
+    if (ii + PD < WR) load_row(ii + PD);
+#pragma unroll
+    for (int r = 0; r < SEG; ++r) {
+      const int i = ii - r * S;
+      if (i < 0 || i > 2) continue;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (i == 0 && j == 0) acc[r][c][0] = acc[r][c][1] = 0.f;
+          hfma2_acc<DT>(acc[r][c][0], acc[r][c][1], raw[ii][c * S + j], W[i * 3 + j]);
+        }
+      if (i == 2) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sink(r, c, acc[r][c][0], acc[r][c][1]);
+      }
+    }
+  }
+}
+
+// Segment lengths of the column-pair DW items (rows per item) and their dispatch.
+template <class F>
+__device__ __forceinline__ void with_seg(int seg, F&& f) {
+  switch (seg) {
+    case 14: f(std::integral_constant<int, 14>()); break;
+    case 8: f(std::integral_constant<int, 8>()); break;
+    case 7: f(std::integral_constant<int, 7>()); break;
+    case 4: f(std::integral_constant<int, 4>()); break;
+    case 2: f(std::integral_constant<int, 2>()); break;
+    default: f(std::integral_constant<int, 1>()); break;
+  }
+}
+template <class F>
+__device__ __forceinline__ void with_act(int act, F&& f) {
+  if (act == FCM_ACT_RELU6) f(std::integral_constant<int, 2>());
+  else if (act == FCM_ACT_RELU) f(std::integral_constant<int, 1>());
+  else f(std::integral_constant<int, 0>());
+}
+
+// fp32 pair (lo, hi) -> folded-BN affine (one FFMA2) -> packed bf16x2 / f16x2 with the activation
+template <int DT, int ACT>
+__device__ __forceinline__ uint32_t epi_act2(float lo, float hi, uint64_t sc2, uint64_t bi2, uint32_t hi_c) {
+  float a, b;
+  f2_unpack(f2_fma(f2_pack(lo, hi), sc2, bi2), a, b);
+  uint32_t h;
+  if constexpr (DT == FCM_BF16) {
+    if constexpr (ACT == 0) asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    else asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    if constexpr (ACT == 2) asm("min.bf16x2 %0, %0, %1;" : "+r"(h) : "r"(hi_c));
+  } else {
+    if constexpr (ACT == 0) asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    else asm("cvt.rn.relu.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    if constexpr (ACT == 2) asm("min.f16x2 %0, %0, %1;" : "+r"(h) : "r"(hi_c));
+  }
+  return h;
+}
+
 // fp32 pair -> packed bf16x2 / f16x2 with the activation: ACT 0 none, 1 relu (free in the
 // convert), 2 relu6 (relu convert + one packed min; 6 is exact in both formats).
 template <int DT, int ACT>
@@ -643,32 +733,38 @@ __device__ __forceinline__ void f2_to_i2(uint64_t v, int32_t& a, int32_t& b) {
   b = static_cast<int32_t>(__float_as_uint(y) - 0x4B400000u);
 }
 
-// Stage the 3x3 DW weights of C channels as scale-folded fp32 pairs [9][cwords] (uint64) plus the
-// bias pairs [cwords], zero past C. Both arrays are read back with ld.shared.u64 per lane.
+// Stage the 3x3 DW weights of C channels for dw3_cols_h: the raw packed weight words [9][cwords]
+// (uint32, 2 channels each) followed by the per-word folded-BN scale pairs [cwords] and bias pairs
+// [cwords] (fp32 pairs as uint64), all zero past C. dw3h_bytes(cwords) bytes.
+constexpr int dw3h_bytes(int cwords) { return 52 * cwords; }
 template <int DT>
-__device__ __forceinline__ void stage_dw3_f2(const void* wdw, const Epi& e, int C, int cwords, uint64_t* wsm2,
-                                             uint64_t* bsm2) {
+__device__ __forceinline__ void stage_dw3_h(const void* wdw, const Epi& e, int C, int cwords, uint32_t* wsm) {
   const uint32_t* g = static_cast<const uint32_t*>(wdw);
   const int cw_real = C / 2;
-  const int n = 10 * cwords;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 9 * cwords; i += blockDim.x) {
     const int t = i / cwords, w = i - t * cwords;
-    const bool v = w < cw_real;
-    const float s0 = (v && e.scale) ? __ldg(e.scale + 2 * w) : (v ? 1.f : 0.f);
-    const float s1 = (v && e.scale) ? __ldg(e.scale + 2 * w + 1) : (v ? 1.f : 0.f);
-    uint64_t r = 0ull;
-    if (t < 9) {
-      if (v) {
-        float lo, hi;
-        f2_unpack(word_to_f2<DT>(__ldg(g + t * cw_real + w)), lo, hi);
-        r = f2_pack(lo * s0, hi * s1);
-      }
-      wsm2[t * cwords + w] = r;
-    } else {
-      if (v && e.bias) r = f2_pack(__ldg(e.bias + 2 * w), __ldg(e.bias + 2 * w + 1));
-      bsm2[w] = r;
-    }
+    wsm[i] = w < cw_real ? __ldg(g + t * cw_real + w) : 0u;
   }
+  uint64_t* sb = reinterpret_cast<uint64_t*>(wsm + 9 * cwords);
+  for (int w = threadIdx.x; w < cwords; w += blockDim.x) {
+    const bool v = w < cw_real;
+    const float s0 = v ? (e.scale ? __ldg(e.scale + 2 * w) : 1.f) : 0.f;
+    const float s1 = v ? (e.scale ? __ldg(e.scale + 2 * w + 1) : 1.f) : 0.f;
+    const float b0 = (v && e.bias) ? __ldg(e.bias + 2 * w) : 0.f;
+    const float b1 = (v && e.bias) ? __ldg(e.bias + 2 * w + 1) : 0.f;
+    sb[w] = f2_pack(s0, s1);
+    sb[cwords + w] = f2_pack(b0, b1);
+  }
+}
+// This lane's word `cw` of the staged weights: 9 packed taps + scale / bias pairs.
+__device__ __forceinline__ void load_dw3_h(const uint32_t* wsm, int cwords, int cw, uint32_t (&W)[9], uint64_t& sc2,
+                                           uint64_t& bi2) {
+  const uint32_t a = smem_u32(wsm) + 4 * cw;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) W[q] = lds32(a + 4 * q * cwords);
+  const uint32_t sa = smem_u32(wsm) + 36 * cwords + 8 * cw;
+  sc2 = lds64(sa);
+  bi2 = lds64(sa + 8 * cwords);
 }
 
 // K-major operand without swizzle (UMMA "interleave" layout): row m of 16-byte channel chunk q at

@@ -162,6 +162,17 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
 __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// A warp group waits for an mbarrier phase: only the leader warp polls (try_wait returns after a
+// short suspend, so every polling warp costs issue slots: measured 16-20 % of a DWPW CTA's
+// instructions with 4 polling epilogue warps); the others block in bar.sync, which issues nothing.
+__device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool leader, uint32_t bar_id,
+                                           uint32_t nthreads);
+
+__device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool leader, uint32_t bar_id,
+                                           uint32_t nthreads) {
+  if (leader) mbar_wait(bar, parity);
+  named_bar_sync(bar_id, nthreads);
+}
 
 // ------------------------------------------------------------------ tcgen05
 template <uint32_t kCols>

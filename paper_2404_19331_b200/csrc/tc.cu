@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(576, 1)
       acc_of(local, acc, ph);
       const int tm = fdiv(t, fnbn);
       const int m0 = tm * 128, n0 = (t - tm * nbn) * BN;
-      mbar_wait_sleep(tfull + acc, ph);
+      group_wait(tfull + acc, ph, hs == 0 && (warp & 3) == 0, 2 + g, 4 * spg * 32);
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
       if (!(dbg & 32))
@@ -334,19 +334,27 @@ __global__ void __launch_bounds__(576, 1)
 // "contains all channels" in time, not space. The PW epilogue stores straight from
 // registers (a lane owns one output pixel: its BN channels are contiguous in NHWC).
 // =====================================================================================
-// DW warps per DWPW CTA (8: the item counts of 128-pixel tiles divide evenly; more warps idle).
-template <int DT, int K> constexpr int dwpw_ndw() { return 8; }
+// DW warps per DWPW CTA
+#ifndef FCM_DWPW_NDW
+#define FCM_DWPW_NDW 8
+#endif
+// 1: a relay warp turns "X stage full + A slot free" into one named-barrier release of all DW
+// warps per C_in chunk; 0: every DW warp waits on the two mbarriers itself (no lock-step)
+#ifndef FCM_DWPW_RELAY
+#define FCM_DWPW_RELAY 1
+#endif
+template <int DT, int K> constexpr int dwpw_ndw() { return FCM_DWPW_NDW; }
 constexpr int kDwpwNA = 2;  // default A-operand (commBuffer) ring depth
 struct DwDivs {
-  FDiv hp, n8, n7, n4;  // column pairs per image, ceil(th / SEG) for SEG = 8, 7, 4
+  FDiv hp;              // column pairs per image
+  FDiv nsg[3];          // ceil(th / SEG) for the SEG of each lane-group width
   FDiv nsplit, tx, ty;  // tile decode
   FDiv thw, tw;         // epilogue: MMA row m -> (image, row, col) of the tile
-  FDiv n14;             // ceil(th / 14)
   int seg_sel;          // SEG per lane-group width: byte g (g = 0, 1, 2 for 32, 16, 8 lanes per slot)
 };
 template <int DT, int K> constexpr bool dwpw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
 template <int DT, int K> constexpr int dwpw_wbytes(int nk) {
-  return dwpw_pair<DT, K>() ? 10 * nk * 32 * 8 : K * K * nk * 32 * 4;
+  return dwpw_pair<DT, K>() ? dw3h_bytes(nk * 32) : K * K * nk * 32 * 4;
 }
 
 template <int DT, int K, int S>
@@ -383,8 +391,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
   uint8_t* cst = bbuf + BS * BN * 128;
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(nk * KC));  // DW weights
-  uint8_t* dscr = reinterpret_cast<uint8_t*>(wsm) + dwpw_wbytes<DT, K>(nk);  // DW warps' dead-row scratch
-  uint64_t* fullX = reinterpret_cast<uint64_t*>(dscr + kDwpwNDW * 128);
+  uint64_t* fullX = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(wsm) + dwpw_wbytes<DT, K>(nk));
   uint64_t* emptyX = fullX + XS;
   uint64_t* fullB = emptyX + XS;
   uint64_t* emptyB = fullB + BS;
@@ -396,8 +403,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cout, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cin, nk * KC, dcst);
-  uint64_t* wsm2 = reinterpret_cast<uint64_t*>(wsm);  // kPair: scale-folded fp32 pairs [9][nk*32], bias [nk*32]
-  if constexpr (kPair) stage_dw3_f2<DT>(wdw, ed, Cin, nk * 32, wsm2, wsm2 + 9 * nk * 32);
+  // kPair: raw packed weight words [9][nk*32] + scale / bias pairs (stage_dw3_h)
+  if constexpr (kPair) stage_dw3_h<DT>(wdw, ed, Cin, nk * 32, wsm);
   else stage_dw_weights<DT>(wdw, K, Cin, nk * 32, wsm);
   for (int i = threadIdx.x; i < na * aslot / 16; i += blockDim.x) sts128(smem_u32(abuf) + 16 * i, 0, 0, 0, 0);
   if (warp == WARP_TX && lane == 0) {
@@ -509,9 +516,22 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           const uint32_t astep = kPair ? (2 * albo) >> 4 : 2;
           const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + sb * BN * 128));
           const int ksteps = min(4, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
-          for (int h = 0; h < MB; ++h)
-            for (int k = 0; k < ksteps && !(dbg & 256); ++k)
-              mma_ss<KIND>(d + h * BN, ad + h * (2048 >> 4) + astep * k, bd + 2 * k, idesc, (kc | k) != 0);
+          // fully unrolled (MB <= 2, ksteps <= 4) with the descriptors formed up front: a rolled loop
+          // serialises the per-MMA vector -> uniform register moves (~160 cycles per MMA measured)
+          if (!(dbg & 256)) {
+            uint64_t adk[2][4], bdk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              bdk[k] = bd + 2 * k;
+              adk[0][k] = ad + astep * k;
+              adk[1][k] = ad + (2048 >> 4) + astep * k;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (h < MB && k < ksteps) mma_ss<KIND>(d + h * BN, adk[h][k], bdk[k], idesc, (kc | k) != 0);
+          }
           mma_commit(aempty + a);
           cstamp(local * nk + kc, 7);
           if (!resB) mma_commit(emptyB + sb);
@@ -523,7 +543,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
   } else if (warp == WARP_RELAY) {
     Ring rx(XS), ra(na);
     int p = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x)
+    for (int t = blockIdx.x; t < total && FCM_DWPW_RELAY; t += gridDim.x)
       for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next(), ++p) {
         mbar_wait(fullX + rx.i, rx.ph);
         if (lane == 0) cstamp(p, 0);
@@ -537,10 +557,20 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     const int dw = warp - 4;
     const int nseg = (th + kSeg - 1) / kSeg;
     const uint32_t hi_c = kPair ? bound2<DT>(act_hi(ed.act)) : 0u;
-    uint64_t W9[9], bias2 = 0ull;
+    uint32_t W9[9];
+    uint64_t sc2 = 0ull, bi2 = 0ull;
     int kc_w = -1;
     Ring rx(XS), ra(na);
     int local = 0, phase = 0;
+    // start of a C_in-chunk phase: X stage full and A slot free (relay barrier or own mbarrier waits)
+    auto go = [&]() {
+      if constexpr (FCM_DWPW_RELAY) {
+        named_bar_sync(2 + (phase & 1), kGoThreads);
+      } else {
+        mbar_wait(fullX + rx.i, rx.ph);
+        mbar_wait(aempty + ra.i, ra.ph ^ 1);
+      }
+    };
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next(), ++phase) {
         const int sx = rx.i, a = ra.i;
@@ -553,59 +583,49 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           const int gi = cw_valid > 16 ? 0 : (cw_valid > 8 ? 1 : 2);
           const int gsl = 5 - gi, npl = gi;
           const int grp = lane >> gsl, wd = lane & ((1 << gsl) - 1);
-          if (kc != kc_w) {  // this chunk's scale-folded weights + bias (once per CTA when nk == 1)
-            const uint32_t wa = smem_u32(wsm2) + 8 * (kc * 32 + wd);
-#pragma unroll
-            for (int q = 0; q < 9; ++q) W9[q] = lds64(wa + q * 8 * nk * 32);
-            bias2 = lds64(wa + 9 * 8 * nk * 32);
+          if (kc != kc_w) {  // this chunk's weights + scale / bias (once per CTA when nk == 1)
+            load_dw3_h(wsm, nk * 32, kc * 32 + wd, W9, sc2, bi2);
             kc_w = kc;
           }
           const uint32_t lane_off = (wd >> 2) * albo + (wd & 3) * 4;
-          const uint32_t dead = smem_u32(dscr) + (dw * 32 + lane) * 4;
           const int hp = (tw + 1) >> 1;   // column pairs per image row
           const int ncp = nb * hp;
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 10);
           if (dw == 0 && lane == 0) cstamp(phase, 2);
-          named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
+          go();
           if (dw == 0 && lane == 0) cstamp(phase, 3);
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 11);
-          // item = (column pair, segment of SEG rows); SEG chosen on the host per lane-group width
-          auto run_items = [&](auto segc, auto actc, FDiv fnsg) {
-            constexpr int SEG = decltype(segc)::value;
-            constexpr int ACT = decltype(actc)::value;
-            const int nsg = (th + SEG - 1) / SEG;
-            const int nit = ncp * nsg;
-            for (int base = dw << npl; base < nit && !(dbg & 1); base += kDwpwNDW << npl) {
-              const int item = base + grp;
-              const bool live = item < nit;
-              const int iv = live ? item : 0;
-              const int cp = fdiv(iv, fnsg), seg = iv - cp * nsg;
-              const int b = fdiv(cp, dv.hp), x0 = 2 * (cp - b * hp);
-              const int y0 = seg * SEG;
-              const uint32_t src = st + (((b * th_in) * tw_in + x0 * S) * 32 + wd) * 4;
-              const int nvalid = live ? th - y0 : 0;
-              const bool c1 = x0 + 1 < tw;
-              const uint32_t a0 = abase + lane_off + (uint32_t)((b * th + y0) * tw + x0) * 16;
-              const uint32_t rstep = (uint32_t)tw * 16;
-              dw3_pair<DT, S, SEG>(src, 128, tw_in * 128, y0, th_in - 1, W9, bias2,
-                                   [&](int r, uint64_t p0, uint64_t p1) {
-                                     const uint32_t ad = a0 + r * rstep;
-                                     const bool rok = r < nvalid;
-                                     sts32(rok ? ad : dead, pack_act<DT, ACT>(p0, hi_c));
-                                     sts32(rok && c1 ? ad + 16 : dead, pack_act<DT, ACT>(p1, hi_c));
-                                   });
-            }
-          };
-          auto run_act = [&](auto segc, FDiv fnsg) {
-            if (ed.act == FCM_ACT_RELU6) run_items(segc, std::integral_constant<int, 2>(), fnsg);
-            else if (ed.act == FCM_ACT_RELU) run_items(segc, std::integral_constant<int, 1>(), fnsg);
-            else run_items(segc, std::integral_constant<int, 0>(), fnsg);
-          };
+          // item = (column pair, segment of SEG rows); SEG (<= th) chosen on the host per lane-group
+          // width. A ragged last segment / odd last column pair is shifted back inside the tile
+          // (y0 = th - SEG, x0 = tw - 2): the overlap is recomputed with identical values, so every
+          // item reads only staged rows and stores unpredicated (slots past the item count excepted)
           const int seg_sel = (dv.seg_sel >> (8 * gi)) & 0xFF;
-          if (seg_sel == 14) run_act(std::integral_constant<int, 14>(), dv.n14);
-          else if (seg_sel == 8) run_act(std::integral_constant<int, 8>(), dv.n8);
-          else if (seg_sel == 7) run_act(std::integral_constant<int, 7>(), dv.n7);
-          else run_act(std::integral_constant<int, 4>(), dv.n4);
+          const FDiv fnsg = gi == 0 ? dv.nsg[0] : (gi == 1 ? dv.nsg[1] : dv.nsg[2]);  // no dynamic param index (-> stack)
+          with_seg(seg_sel, [&](auto segc) {
+            constexpr int SEG = decltype(segc)::value;
+            with_act(ed.act, [&](auto actc) {
+              constexpr int ACT = decltype(actc)::value;
+              const int nsg = (th + SEG - 1) / SEG;
+              const int nit = ncp * nsg;
+              const uint32_t rstep = (uint32_t)tw * 16;
+              for (int base = dw << npl; base < nit && !(dbg & 1); base += kDwpwNDW << npl) {
+                const int item = base + grp;
+                const bool live = item < nit;
+                const int iv = live ? item : 0;
+                const int cp = fdiv(iv, fnsg), seg = iv - cp * nsg;
+                const int b = fdiv(cp, dv.hp);
+                const int x0 = max(0, min(2 * (cp - b * hp), tw - 2));
+                const int y0 = min(seg * SEG, th - SEG);
+                const uint32_t src = st + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * 32 + wd) * 4;
+                const bool p1 = live && x0 + 1 < tw;
+                const uint32_t a0 = abase + lane_off + (uint32_t)((b * th + y0) * tw + x0) * 16;
+                dw3_cols_h<DT, S, SEG, 2, 128>(src, tw_in * 128, W9, [&](int r, int c, float lo, float hi) {
+                  const uint32_t v = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
+                  if (c == 0 ? live : p1) sts32(a0 + r * rstep + c * 16, v);
+                });
+              }
+            });
+          });
         } else {
          bool done = false;
          if constexpr (DT == FCM_S8 && K == 3) {
@@ -642,7 +662,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             }
           }
           const int zp = ed.zp_out, qmin = ed.qmin, qmax = ed.qmax;
-          named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
+          go();
           const int ncolp = (tw + 1) >> 1;
           const int ncg = (nb * ncolp + npix - 1) / npix;
           for (int item = dw; item < ncg * nseg; item += kDwpwNDW) {
@@ -687,7 +707,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           EpiC ec[V];
 #pragma unroll
           for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, cl + v);
-          named_bar_sync(2 + (phase & 1), kGoThreads);  // relay: X stage full and A slot free
+          go();
           const int ncolg = (nb * tw + npix - 1) / npix;
           for (int item = dw; item < ncolg * nseg; item += kDwpwNDW) {
             const int cg = item / nseg, seg = item - cg * nseg;
@@ -729,7 +749,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
       int ns, nbi, tyi, txi;
       decode(t, ns, nbi, tyi, txi);
       const int valid = min(BN, Cout - ns * BN);
-      mbar_wait_sleep(tfull + acc, rt.ph);
+      group_wait(tfull + acc, rt.ph, warp == 0, 4, 128);
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
       for (int h = 0; h < MB && !(dbg & 2); ++h) {
@@ -803,7 +823,7 @@ struct PwdwDivs {
 };
 template <int DT, int K> constexpr bool pwdw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
 template <int DT, int K> constexpr int pwdw_wbytes(int nslice) {
-  return pwdw_pair<DT, K>() ? 10 * nslice * 32 * 8 : K * K * nslice * 128;
+  return pwdw_pair<DT, K>() ? dw3h_bytes(nslice * 32) : K * K * nslice * 128;
 }
 
 template <int DT, int K, int S>
@@ -851,8 +871,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cmid, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cmid, ncap, dcst);
-  uint64_t* wsm2 = reinterpret_cast<uint64_t*>(wsm);  // pair core: scale-folded fp32 pairs [9][nslice*32] + bias
-  if constexpr (pwdw_pair<DT, K>()) stage_dw3_f2<DT>(wdw, ed, Cmid, nslice * 32, wsm2, wsm2 + 9 * nslice * 32);
+  // pair core: raw packed weight words [9][nslice*32] + scale / bias pairs (stage_dw3_h)
+  if constexpr (pwdw_pair<DT, K>()) stage_dw3_h<DT>(wdw, ed, Cmid, nslice * 32, wsm);
   else stage_dw_weights<DT>(wdw, K, Cmid, nslice * 32, wsm);
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch_desc(&tmx);
@@ -960,10 +980,13 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       uint8_t* tb = tsm + acc * tbytes;
-      mbar_wait_sleep(tfull + acc, (local / depth) & 1);
-      if (warp == 0 && lane == 0) stamp(local, 3);
-      mbar_wait(Tempty + acc, ((local / depth) & 1) ^ 1);
-      if (warp == 0 && lane == 0) stamp(local, 4);
+      if (warp == 0) {
+        mbar_wait(tfull + acc, (local / depth) & 1);
+        if (lane == 0) stamp(local, 3);
+        mbar_wait(Tempty + acc, ((local / depth) & 1) ^ 1);
+        if (lane == 0) stamp(local, 4);
+      }
+      named_bar_sync(2, NTP * 32);
       tc_fence_after();
       for (int mb = 0; mb < MB && !(dbg & 2); ++mb) {
         const int r = mb * 128 + q * 32 + lane;
@@ -1004,7 +1027,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     const int nitems = nb * tw * nseg;
     const uint32_t hi_c = bound2<DT>(act_hi(ed.act));
     uint32_t* yw = reinterpret_cast<uint32_t*>(y);
-    uint64_t W9[9], bias2 = 0ull;
+    uint32_t W9[9];
+    uint64_t sc2 = 0ull, bi2 = 0ull;
     int sl_w = -1;
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -1018,57 +1042,48 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       if constexpr (kPair) {
         // column-pair FFMA2 core (as in DWPW): a lane owns one channel word of 2 adjacent output
         // columns x SEG rows; stores go straight to the NHWC OFM (128 B per warp and pixel)
-        if (sl != sl_w) {  // this slice's weights / bias (once per CTA with resident slices)
-          const uint32_t wa = smem_u32(wsm2) + 8 * (sl * 32 + lane);
-#pragma unroll
-          for (int q = 0; q < 9; ++q) W9[q] = lds64(wa + q * 8 * nslice * 32);
-          bias2 = lds64(wa + 9 * 8 * nslice * 32);
+        if (sl != sl_w) {  // this slice's weights / scale / bias (once per CTA with resident slices)
+          load_dw3_h(wsm, nslice * 32, sl * 32 + lane, W9, sc2, bi2);
           sl_w = sl;
         }
         const bool cval = c < Cmid;
         const int hp = (tw + 1) >> 1;
-        mbar_wait(Tfull + tbi, (local / depth) & 1);
+        group_wait(Tfull + tbi, (local / depth) & 1, dw == 0, 3, kPwdwNDW * 32);
         if (dw == 0 && lane == 0) stamp(local, 6);
-        auto run = [&](auto segc, auto actc) {
+        with_seg(dv.seg, [&](auto segc) {
           constexpr int SEG = decltype(segc)::value;
-          constexpr int ACT = decltype(actc)::value;
-          const int nsg = (th + SEG - 1) / SEG;
-          const int nit = nb * hp * nsg;
-          for (int item = dw; item < nit && !(dbg & 1); item += kPwdwNDW) {
-            const int cp = fdiv(item, dv.nsg), seg = item - cp * nsg;
-            const int b = fdiv(cp, dv.hp), x0 = 2 * (cp - b * hp);
-            const int n = nbi * nb + b, xo = txi * tw + x0;
-            const int y0 = seg * SEG;
-            if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
-            const uint32_t src = tsa + (((b * th_in) * tw_in + x0 * S) * PW + lane) * 4;
-            const int nvalid = nrows_t - y0;
-            const bool c0ok = cval, c1ok = cval && (x0 + 1 < tw) && (xo + 1 < Wo);
-            uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
-            const size_t rstride = (size_t)Wo * Cmid / V, cstride = (size_t)Cmid / V;
-            dw3_pair<DT, S, SEG>(src, PITCH, tw_in * PITCH, y0, th_in - 1, W9, bias2,
-                                 [&](int r, uint64_t p0, uint64_t p1) {
-                                   const bool rok = r < nvalid;
-                                   if (rok && c0ok) dst[r * rstride] = pack_act<DT, ACT>(p0, hi_c);
-                                   if (rok && c1ok) dst[r * rstride + cstride] = pack_act<DT, ACT>(p1, hi_c);
-                                 });
-          }
-        };
-        auto run_act = [&](auto segc) {
-          if (ed.act == FCM_ACT_RELU6) run(segc, std::integral_constant<int, 2>());
-          else if (ed.act == FCM_ACT_RELU) run(segc, std::integral_constant<int, 1>());
-          else run(segc, std::integral_constant<int, 0>());
-        };
-        if (dv.seg == 14) run_act(std::integral_constant<int, 14>());
-        else if (dv.seg == 8) run_act(std::integral_constant<int, 8>());
-        else if (dv.seg == 7) run_act(std::integral_constant<int, 7>());
-        else run_act(std::integral_constant<int, 4>());
+          with_act(ed.act, [&](auto actc) {
+            constexpr int ACT = decltype(actc)::value;
+            const int nsg = (th + SEG - 1) / SEG;
+            const int nit = nb * hp * nsg;
+            for (int item = dw; item < nit && !(dbg & 1); item += kPwdwNDW) {
+              // ragged last segment / odd last column pair shifted back inside the tile (SEG <= th):
+              // the overlap is recomputed and stored twice with identical values
+              const int cp = fdiv(item, dv.nsg), seg = item - cp * nsg;
+              const int b = fdiv(cp, dv.hp);
+              const int x0 = max(0, min(2 * (cp - b * hp), tw - 2));
+              const int n = nbi * nb + b, xo = txi * tw + x0;
+              const int y0 = min(seg * SEG, th - SEG);
+              if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
+              const uint32_t src = tsa + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * PW + lane) * 4;
+              const int nvalid = nrows_t - y0;
+              const bool c0ok = cval, c1ok = cval && (x0 + 1 < tw) && (xo + 1 < Wo);
+              uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
+              const size_t rstride = (size_t)Wo * Cmid / V, cstride = (size_t)Cmid / V;
+              dw3_cols_h<DT, S, SEG, 2, PITCH>(src, tw_in * PITCH, W9, [&](int r, int cc, float lo, float hi) {
+                if (r < nvalid && (cc == 0 ? c0ok : c1ok))
+                  dst[r * rstride + cc * cstride] = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
+              });
+            }
+          });
+        });
       } else {
         DwW<DT, K> Wd;
         load_dw_weights_smem<DT, K>(Wd, wsm, nslice * 32, sl * 32 + lane);
         EpiC ec[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
-        mbar_wait(Tfull + tbi, (local / depth) & 1);
+        group_wait(Tfull + tbi, (local / depth) & 1, dw == 0, 3, kPwdwNDW * 32);
         for (int item = dw; item < nitems; item += kPwdwNDW) {
           const int col = fdiv(item, dv.nseg), seg = item - col * nseg;
           const int b = fdiv(col, dv.tw), x = col - b * tw;
@@ -1231,21 +1246,29 @@ template <int K, int S>
 static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
   const int hp = (g.tw + 1) / 2;
   int sel = 0;
+  DwDivs d{};
   for (int gi = 0; gi < 3; ++gi) {
     const int slots = 1 << gi;
-    int best = 0, bcost = 1 << 30;
-    for (int seg : {14, 8, 7, 4}) {
+    int best = 1, bcost = 1 << 30;
+    for (int seg : {14, 8, 7, 4, 2, 1}) {
+      if (seg > g.th) continue;  // a segment never leaves the tile (ragged segments shift up)
       const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
       const int rounds = ((nit + slots - 1) / slots + ndw - 1) / ndw;
       const int cost = rounds * ((seg - 1) * S + K + 2);
       if (cost < bcost) { bcost = cost; best = seg; }
     }
     sel |= best << (8 * gi);
+    d.nsg[gi] = make_fdiv((g.th + best - 1) / best);
   }
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
-  return DwDivs{make_fdiv(hp),      make_fdiv((g.th + 7) / 8), make_fdiv((g.th + 6) / 7), make_fdiv((g.th + 3) / 4),
-                make_fdiv(nsplit), make_fdiv(tiles_x),        make_fdiv(tiles_y),        make_fdiv(g.th * g.tw),
-                make_fdiv(g.tw),   make_fdiv((g.th + 13) / 14), sel};
+  d.hp = make_fdiv(hp);
+  d.nsplit = make_fdiv(nsplit);
+  d.tx = make_fdiv(tiles_x);
+  d.ty = make_fdiv(tiles_y);
+  d.thw = make_fdiv(g.th * g.tw);
+  d.tw = make_fdiv(g.tw);
+  d.seg_sel = sel;
+  return d;
 }
 
 template <int DT, int K, int S>
@@ -1260,7 +1283,8 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
     return set_error(FCM_E_INFEASIBLE, "dwpw: tile has more pixels than the MMA rows (256 pair core, else 128)");
   if (th_in > 256 || tw_in > 256 || g.nb > 256) return set_error(FCM_E_INFEASIBLE, "dwpw: halo box > 256");
   const int MB = (tpx + 127) / 128;            // MMA row blocks of 128
-  const int albo = 16 * 128 * MB + 16;          // interleave LBO (padded: conflict-free DW stores)
+  static const int albo_pad = [] { const char* e = getenv("FCM_ALBO_PAD"); return e ? atoi(e) : 16; }();  // dev
+  const int albo = 16 * 128 * MB + albo_pad;    // interleave LBO (padded: conflict-free DW stores)
   int nsplit = 0;
   const int BN = pick_bn<DT>(g.Cout, nsplit_req, nsplit);
   if (2 * MB * BN > 512) return set_error(FCM_E_INFEASIBLE, "dwpw: 2 x (tile rows / 128) x C_out slice > 512 TMEM columns");
@@ -1285,8 +1309,7 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   const int na = na_env ? na_env : kDwpwNA;
   const int nacc = 2;
   const int aslot = kPair ? ((8 * albo + 1023) & ~1023) : 16384;
-  const int fixed = 1024 + na * aslot + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + dwpw_wbytes<DT, K>(nk) +
-                    dwpw_ndw<DT, K>() * 128 + 512;
+  const int fixed = 1024 + na * aslot + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + dwpw_wbytes<DT, K>(nk) + 512;
   const int xstride = ((g.nb * th_in * tw_in * 128) + 1023) & ~1023;
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nsplit;
@@ -1345,8 +1368,9 @@ int launch_dwpw_tc(int dt, const void* x, const void* wdw, const Epi& ed, const 
 template <int DT, int K, int S>
 static PwdwDivs pwdw_divs(const Geo& g, int nslice, int tiles_x, int tiles_y) {
   const int hp = (g.tw + 1) / 2;
-  int best = 4, bcost = 1 << 30;
-  for (int seg : {14, 8, 7, 4}) {
+  int best = 1, bcost = 1 << 30;
+  for (int seg : {14, 8, 7, 4, 2, 1}) {
+    if (seg > g.th) continue;  // segments never leave the tile (ragged ones shift up)
     const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
     const int rounds = (nit + kPwdwNDW - 1) / kPwdwNDW;
     const int cost = rounds * ((seg - 1) * S + K + 2);
@@ -1595,12 +1619,13 @@ __global__ void __launch_bounds__(608, 1)
     uint32_t ph_a1 = 0, ph_f = 0;
     bool first = true;
     for (int t = blockIdx.x; t < nbm; t += gridDim.x) {
-      mbar_wait_sleep(acc1full, ph_a1);
-      ph_a1 ^= 1;
-      if (!first) {  // GEMM2 of the previous tile has finished reading T
-        mbar_wait(tfree, ph_f);
-        ph_f ^= 1;
+      if (warp == 0) {
+        mbar_wait(acc1full, ph_a1);
+        if (!first) mbar_wait(tfree, ph_f);  // GEMM2 of the previous tile has finished reading T
       }
+      named_bar_sync(2, 128);
+      ph_a1 ^= 1;
+      if (!first) ph_f ^= 1;
       first = false;
       tc_fence_after();
       for (int c0 = 0; c0 < nk2 * KC; c0 += 16) {
@@ -1628,7 +1653,7 @@ __global__ void __launch_bounds__(608, 1)
     int sbuf = 0;
     for (int t = blockIdx.x; t < nbm; t += gridDim.x) {
       for (int j = 0; j < nbn2; ++j, ra.next()) {
-        mbar_wait_sleep(acc2full + ra.i, ra.ph);
+        group_wait(acc2full + ra.i, ra.ph, warp == 4, 3, 12 * 32);
         tc_fence_after();
         epilogue_tile_warp<DT>(tacc2 + ra.i * BN2, BN2, j * BN2, N, cs2, ep2, stage + w2i * 4096, sbuf, hs, 3,
                                [&](const uint8_t* buf, int c, int rr) { tma_store_2d(&tmy, buf, c, t * 128 + rr); });

@@ -66,7 +66,8 @@ inline long dwpw_pair_cost(const Geo& g, int nb, int th, int tw, int sms = 148) 
   const long tiles = (long)((g.N + nb - 1) / nb) * ((g.Ho + th - 1) / th) * ((g.Wo + tw - 1) / tw);
   const int hp = (tw + 1) / 2;
   long best = -1;
-  for (int seg : {14, 8, 7, 4}) {
+  for (int seg : {14, 8, 7, 4, 2, 1}) {
+    if (seg > th) continue;
     const int items = nb * hp * ((th + seg - 1) / seg);
     const long t = (long)((items + 7) / 8) * ((seg - 1) * g.s + 3 + 2);
     if (best < 0 || t < best) best = t;
@@ -115,7 +116,7 @@ inline bool pwdw_smem_fits(int dt, const Geo& g, int smem_optin = 232448) {
   const long ncap = (long)(g.Cout + td - 1) / td * td, nslice = ncap / td;
   const long consts = (dt == FCM_S8 ? 12 : 8) * ncap;
   const bool pair = (dt == FCM_BF16 || dt == FCM_F16) && g.k == 3;
-  const long wbytes = pair ? 10 * nslice * 32 * 8 : (long)g.k * g.k * nslice * 128;
+  const long wbytes = pair ? 52 * nslice * 32 : (long)g.k * g.k * nslice * 128;  // dw3h_bytes
   const long fixed = 1024 + 2 * consts + wbytes + 512;
   return fixed + 2 * tbytes + 2 * (mb * 16384 + td * 128) <= smem_optin;
 }

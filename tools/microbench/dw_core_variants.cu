@@ -7,6 +7,13 @@
 //   V2  lane = output pixel, a warp owns one 8-channel octet (TMA inner box = 16 B): 3 LDS.128 per
 //       input row, the fp32 weights come from the kernel-parameter constant bank at a warp-uniform
 //       index (LDCU -> uniform-register FFMA2 operand)
+//   V3  dw3_cols_h, 2 columns: lane = channel word, mixed FHFMA taps straight from the packed words
+//       (no bf16 -> fp32 widening), scale / bias / RELU6 in the sink
+//   V4  dw3_cols_h, 4 columns
+//   V6  V5 with a CTA barrier after every item (all DW warps in lock-step, as in the kernel's
+//       C_in-chunk phases)
+//   V5  V3 with the kernel's runtime geometry: row pitch and output row step are kernel arguments,
+//       stores predicated per item (as in dwpw_tc_kernel)
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
@@ -45,7 +52,8 @@ __device__ __forceinline__ void quad_core(uint32_t src, int row_bytes, const uin
 }
 
 template <int V, int SEG>
-__global__ void k(const __grid_constant__ WP wp, int iters, uint32_t* out) {
+__global__ void k(const __grid_constant__ WP wp, int iters, uint32_t* out, int rb = 40 * 128, int maxr = 19,
+                  int rstep = 512, int nvalid_rt = 64) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x)
@@ -55,7 +63,36 @@ __global__ void k(const __grid_constant__ WP wp, int iters, uint32_t* out) {
   const uint32_t hi2 = 0x40c040c0u;
   const float lf = 0.001f * lane;
   long long t0 = clock64();
-  if constexpr (V == 0 || V == 1) {
+  if constexpr (V == 5 || V == 6) {
+    uint32_t W[9];
+    for (int q = 0; q < 9; ++q) W[q] = 0x3dcc3dccu + q * 0x00010001u + lane;
+    const uint64_t sc2 = f2_pack(1.0f + lf, 0.9f - lf), bi2 = f2_pack(0.5f + lf, 0.25f - lf);
+    for (int it = 0; it < iters; ++it) {
+      const int x0 = 2 * ((warp + it) & 7), y0 = SEG > 8 ? 0 : ((warp >> 3) + it) & 1;
+      const uint32_t src = xt + ((y0 * 40 + x0) * 32 + lane) * 4;
+      const uint32_t a0 = ab + (lane >> 2) * kAlbo + (lane & 3) * 4 + (uint32_t)(y0 * 32 + x0) * 16;
+      const int nvalid = nvalid_rt - y0;
+      const bool c1 = x0 + 1 < 40;
+      dw3_cols_h<FCM_BF16, 1, SEG, 2, 128>(src, rb, W, [&](int r, int c, float lo, float hi) {
+        const uint32_t v = epi_act2<FCM_BF16, 2>(lo, hi, sc2, bi2, hi2);
+        if (c == 0 ? nvalid > 0 : c1) sts32(a0 + r * rstep + c * 16, v);
+      });
+      if constexpr (V == 6) __syncthreads();
+    }
+  } else if constexpr (V == 3 || V == 4) {
+    constexpr int NC = V == 3 ? 2 : 4;
+    uint32_t W[9];
+    for (int q = 0; q < 9; ++q) W[q] = 0x3dcc3dccu + q * 0x00010001u + lane;
+    const uint64_t sc2 = f2_pack(1.0f + lf, 0.9f - lf), bi2 = f2_pack(0.5f + lf, 0.25f - lf);
+    for (int it = 0; it < iters; ++it) {
+      const int x0 = NC * ((warp + it) & 7), y0 = SEG > 8 ? 0 : ((warp >> 3) + it) & 1;
+      const uint32_t src = xt + ((y0 * 40 + x0) * 32 + lane) * 4;
+      const uint32_t a0 = ab + (lane >> 2) * kAlbo + (lane & 3) * 4 + (uint32_t)(y0 * 32 + x0) * 16;
+      dw3_cols_h<FCM_BF16, 1, SEG, NC, 128>(src, 40 * 128, W, [&](int r, int c, float lo, float hi) {
+        sts32(a0 + r * 512 + c * 16, epi_act2<FCM_BF16, 2>(lo, hi, sc2, bi2, hi2));
+      });
+    }
+  } else if constexpr (V == 0 || V == 1) {
     uint64_t W[9];
     for (int q = 0; q < 9; ++q) W[q] = f2_pack(0.1f * q + lf, 0.2f * q - lf);
     const uint64_t bias = f2_pack(0.5f + lf, 0.25f - lf);
@@ -133,7 +170,7 @@ int main() {
     const int iters = 1024;
     for (int rep = 0; rep < 2; ++rep) {
       for (int i = 0; i < 64; ++i) o[i] = 0;
-      kern<<<148, nw * 32, 160 * 1024>>>(wp, iters, o);
+      kern<<<148, nw * 32, 160 * 1024>>>(wp, iters, o, 40 * 128, 19, 512, 64);
       cudaError_t e = cudaDeviceSynchronize();
       double cyc = 0;
       for (int w = 0; w < nw; ++w) cyc = cyc > o[w] ? cyc : o[w];
@@ -150,6 +187,14 @@ int main() {
     run(k<1, 6>, "V1 quad (lane=word, 4 col), SEG 6", nw, 4 * 6 * 64);
     run(k<1, 8>, "V1 quad (lane=word, 4 col), SEG 8", nw, 4 * 8 * 64);
     run(k<2, 4>, "V2 pixel (lane=px, UR W), SEG 4", nw, 32 * 4 * 8);
+    run(k<3, 8>, "V3 FHFMA pair, SEG 8", nw, 2 * 8 * 64);
+    run(k<3, 14>, "V3 FHFMA pair, SEG 14", nw, 2 * 14 * 64);
+    run(k<5, 14>, "V5 FHFMA pair runtime geometry, SEG 14", nw, 2 * 14 * 64);
+    run(k<5, 8>, "V5 FHFMA pair runtime geometry, SEG 8", nw, 2 * 8 * 64);
+    run(k<6, 14>, "V6 = V5 + barrier per item, SEG 14", nw, 2 * 14 * 64);
+    run(k<3, 4>, "V3 FHFMA pair, SEG 4", nw, 2 * 4 * 64);
+    run(k<4, 4>, "V4 FHFMA quad, SEG 4", nw, 4 * 4 * 64);
+    run(k<4, 8>, "V4 FHFMA quad, SEG 8", nw, 4 * 8 * 64);
     run(k<2, 6>, "V2 pixel (lane=px, UR W), SEG 6", nw, 32 * 6 * 8);
   }
   return 0;
