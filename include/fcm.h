@@ -17,8 +17,8 @@
  *   DW  O[n,y,x,c]  = eps_c( sum_{i,j<k} X[n, y*s-pad_t+i, x*s-pad_l+j, c] * Wdw[i][j][c] ),
  *                     out-of-image taps contribute 0; Ho = (H+pad_t+pad_b-k)/s + 1 (floor).
  *   PW  O[p,co]     = eps_co( sum_ci X[p,ci] * Wpw[ci][co] ) for every pixel p.
- *   eps (float)     v = acc*scale[c] + bias[c]; NONE | RELU | RELU6; round-to-nearest-even
- *                     to the output dtype (scale/bias NULL -> 1 / 0).
+ *   eps (float)     v = acc*scale[c] + bias[c]; NONE | RELU | RELU6 | SILU | GELU; + residual
+ *                     (optional); round-to-nearest-even to the output dtype (scale/bias NULL -> 1 / 0).
  *   eps (int8)      r = ((acc + bias_q[c]) * mult_q[c] + 2^(shift_q[c]-1)) >> shift_q[c]
  *                     (64-bit product, arithmetic shift) + zp_out, clamped to [qmin, qmax].
  *                     acc = sum (q - zp_in) * w, int32. RELU/RELU6 are encoded by qmin/qmax.
@@ -86,6 +86,8 @@ extern "C" {
 #define FCM_ACT_NONE 0
 #define FCM_ACT_RELU 1
 #define FCM_ACT_RELU6 2
+#define FCM_ACT_SILU 3 /* v * sigmoid(v) (EfficientNet); float paths only */
+#define FCM_ACT_GELU 4 /* 0.5 v (1 + erf(v / sqrt 2)) (CeiT / CMT); float paths only */
 
 /* A dense 4-D activation tensor in device memory. n,h,w,c are logical dims (any layout). */
 typedef struct {
@@ -102,7 +104,12 @@ typedef struct {
 } fcm_dw_geom;
 
 /* Conv-Norm-Activation epilogue. Float paths use act/scale/bias; int8 uses the
- * quantised fields (bias_q, mult_q, shift_q, zp_in, zp_out, qmin, qmax). Device pointers. */
+ * quantised fields (bias_q, mult_q, shift_q, zp_in, zp_out, qmin, qmax). Device pointers.
+ * residual (optional, NULL = none, the inverted-residual / MBConv / IRFFN
+ * shortcut): a tensor of the OUTPUT's shape and dtype (NHWC, dense) added after the
+ * activation, y = round(act(acc*scale + bias) + residual). Float dtypes only, and only on the
+ * epilogue that writes a call's output through a pointwise conv: fcm_pw, fcm_dwpw's ep_pw,
+ * fcm_pwpw's ep2 (elsewhere FCM_E_UNSUPPORTED). It may not overlap the output. */
 typedef struct {
   int32_t act;
   const float* scale;
@@ -111,6 +118,7 @@ typedef struct {
   const int32_t* mult_q;
   const int32_t* shift_q;
   int32_t zp_in, zp_out, qmin, qmax;
+  const void* residual;
 } fcm_epilogue;
 
 /* Optional tile override (NULL = the library's default for the shape). Output-space tile

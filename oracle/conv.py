@@ -8,8 +8,13 @@ Definitions (§II-B; readings R1-R
   PW  O[p,co]     = eps_co( sum_ci X[p,ci] * Wpw[ci,co] )  for every pixel p
                     ("1x1 filters span over all channels")
   eps             Conv-Norm-Activation epilogue: folded-BN scale/bias, then
-                    NONE / RELU / RELU6, then rounding to the storage format. int8: int32 bias,
-                    fixed-point requantisation, + zero point, clamp [qmin, qmax] (reading R1).
+                    NONE / RELU / RELU6 / SILU / GELU, then the optional residual (shortcut) add,
+                    then rounding to the storage format. int8: int32 bias, fixed-point
+                    requantisation, + zero point, clamp [qmin, qmax] (reading R1).
+                    SILU (EfficientNet's swish) = v * sigmoid(v) = v / (1 + e^-v); GELU (CeiT / CMT)
+                    = v * Phi(v) = 0.5 v (1 + erf(v / sqrt 2)); the residual is the inverted-residual
+                    / MBConv / IRFFN shortcut ("inverted residual"); SURVEY §8(f) rank 4,
+                    readings R4 / R24 in DESIGN.md.
   DWPW            = PW(DW(X)): the intermediate T is materialised in the feature-map dtype
                     (P:111 'fms_dt commBuffer'; P:144 int8 packed before writing ANY buffer).
   PWDW / PWDW_R   = DW(PW(X)): DW pads T, not X -- an out-of-image tap of T is the real 0
@@ -22,10 +27,11 @@ Accumulation in float64 (products of <=24-bit significands are exact) / exact in
 from __future__ import annotations
 
 import numpy as np
+from scipy.special import erf
 
 from oracle.numerics import requant, round_to
 
-ACT_NONE, ACT_RELU, ACT_RELU6 = 0, 1, 2
+ACT_NONE, ACT_RELU, ACT_RELU6, ACT_SILU, ACT_GELU = 0, 1, 2, 3, 4
 
 
 def out_size(h: int, k: int, s: int, p0: int, p1: int) -> int:
@@ -58,6 +64,11 @@ def act_float(v: np.ndarray, act: int) -> np.ndarray:
         return np.maximum(v, 0.0)
     if act == ACT_RELU6:
         return np.minimum(np.maximum(v, 0.0), 6.0)
+    if act == ACT_SILU:
+        with np.errstate(over="ignore"):
+            return v / (1.0 + np.exp(-v))
+    if act == ACT_GELU:
+        return 0.5 * v * (1.0 + erf(v / np.sqrt(2.0)))
     return v
 
 
@@ -65,7 +76,10 @@ def epilogue_float(acc: np.ndarray, p: dict, fmt: str) -> np.ndarray:
     scale = p.get("scale")
     bias = p.get("bias")
     v = acc * (1.0 if scale is None else scale) + (0.0 if bias is None else bias)
-    return round_to(act_float(v, p.get("act", ACT_NONE)), fmt)
+    v = act_float(v, p.get("act", ACT_NONE))
+    if p.get("residual") is not None:
+        v = v + p["residual"]
+    return round_to(v, fmt)
 
 
 def epilogue_int8(acc: np.ndarray, p: dict) -> np.ndarray:
@@ -112,7 +126,8 @@ def _absp(p):
     q = dict(p)
     q["scale"] = None if p.get("scale") is None else np.abs(p["scale"])
     q["bias"] = None if p.get("bias") is None else np.abs(p["bias"])
-    q["act"] = ACT_NONE
+    q["act"] = ACT_NONE  # |relu(v)|, |silu(v)|, |gelu(v)| <= |v| (the latter two up to 1.13 |dv| slope)
+    q["residual"] = None if p.get("residual") is None else np.abs(p["residual"])
     return q
 
 

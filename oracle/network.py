@@ -51,7 +51,7 @@ def forward(net, dtype, n0, n, seed=synth.SEED, prm=None, keep=False):
     first = ids[0][2]
     c0 = first["c"] if first["kind"] == "dw" else first["c_in"]
     x0 = _images(net, dtype, f"{net}/input", n0, n, first["h"], first["w"], c0, seed)
-    cur, outs, stage = x0, {}, {}
+    cur, outs, stage, inputs = x0, {}, {}, {}
     for lid, bi, l in ids:
         if lid.endswith(".0"):
             kind, role = block_source(net, blocks, bi)
@@ -60,7 +60,10 @@ def forward(net, dtype, n0, n, seed=synth.SEED, prm=None, keep=False):
                 if role not in stage:
                     stage[role] = x0 if bi == 0 else _images(net, dtype, role, n0, n, l["h"], l["w"], c, seed)
                 cur = stage[role]
+        inputs[lid] = cur
         p = prm[lid]
+        if l.get("residual_from") is not None and dtype != "s8":  # shortcut (float only)
+            p = dict(p, residual=inputs[l["residual_from"]])
         if l["kind"] == "dw":
             k = l["k"]
             cur = conv.dw(cur, p["w"], l["stride"], (k // 2,) * 4, p, dtype)

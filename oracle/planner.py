@@ -185,7 +185,17 @@ def pw_units(M, ci, co, bm, ns):
 
 def b200_numbers(op, layers, N, dtype, tile):
     """Compulsory HBM bytes, exact L2->SM bytes and MACs of one candidate at the
-    tile it reports (tile_n, tile_h, tile_w, n_split)."""
+    tile it reports (tile_n, tile_h, tile_w, n_split). A last layer with a residual (shortcut)
+    epilogue also reads one output-shaped tensor."""
+    out = _b200_numbers(op, layers, N, dtype, tile)
+    last = layers[-1]
+    if last.get("residual"):
+        Ho, Wo = out_hw(last)
+        out["dram_bytes"] += N * Ho * Wo * last["c_out"] * ESZ[dtype]
+    return out
+
+
+def _b200_numbers(op, layers, N, dtype, tile):
     b = ESZ[dtype]
     nb, th, tw, ns = tile["tile_n"], tile["tile_h"], tile["tile_w"], tile["n_split"]
     if op == "dw":
@@ -247,7 +257,7 @@ def fusable(layers, edges):
     ids = [l["id"] for l in layers]
     if edges is None:
         edges = [[ids[i - 1], ids[i]] for i in range(1, n)]
-    outd, ind = {i: 0 for i in ids}, {i: 0 for i in ids}
+    outd, ind = {l["id"]: l.get("extra_consumers", 0) for l in layers}, {i: 0 for i in ids}  # + residual readers
     es = set()
     for a, c in edges:
         outd[a] += 1

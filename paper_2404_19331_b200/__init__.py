@@ -52,10 +52,11 @@ class Epilogue:
     zp_out: int = 0
     qmin: int = -128
     qmax: int = 127
+    residual: Optional[torch.Tensor] = None  # output-shaped shortcut added after the activation (float dtypes)
 
     def c(self) -> L.FcmEpilogue:
         return L.FcmEpilogue(self.act, _ptr(self.scale), _ptr(self.bias), _ptr(self.bias_q), _ptr(self.mult_q),
-                             _ptr(self.shift_q), self.zp_in, self.zp_out, self.qmin, self.qmax)
+                             _ptr(self.shift_q), self.zp_in, self.zp_out, self.qmin, self.qmax, _ptr(self.residual))
 
 
 def _geom(k: int, stride: int, pads: Optional[Sequence[int]]) -> L.FcmDwGeom:

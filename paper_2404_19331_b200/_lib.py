@@ -10,7 +10,7 @@ LIB_PATH = os.environ.get("FCM_LIB_PATH") or os.path.join(_HERE, "libfcm.so")  #
 FCM_OK, FCM_E_INVAL, FCM_E_ALIGN, FCM_E_UNSUPPORTED, FCM_E_INFEASIBLE, FCM_E_CUDA, FCM_E_BUFSZ = 0, -1, -2, -3, -4, -5, -6
 FCM_F32, FCM_BF16, FCM_F16, FCM_S8 = 0, 1, 2, 3
 FCM_NHWC, FCM_NCHW = 0, 1
-ACT_NONE, ACT_RELU, ACT_RELU6 = 0, 1, 2
+ACT_NONE, ACT_RELU, ACT_RELU6, ACT_SILU, ACT_GELU = 0, 1, 2, 3, 4
 
 EXPORTS = ["fcm_dw", "fcm_pw", "fcm_dwpw", "fcm_pwdw_r", "fcm_pwpw", "fcm_pack_pw_bytes", "fcm_pack_pw", "fcm_plan",
            "fcm_launch_count", "fcm_status_str", "fcm_last_error", "fcm_version"]
@@ -29,7 +29,7 @@ class FcmDwGeom(C.Structure):
 class FcmEpilogue(C.Structure):
     _fields_ = [("act", C.c_int32), ("scale", C.c_void_p), ("bias", C.c_void_p), ("bias_q", C.c_void_p),
                 ("mult_q", C.c_void_p), ("shift_q", C.c_void_p), ("zp_in", C.c_int32), ("zp_out", C.c_int32),
-                ("qmin", C.c_int32), ("qmax", C.c_int32)]
+                ("qmin", C.c_int32), ("qmax", C.c_int32), ("residual", C.c_void_p)]
 
 
 class FcmTile(C.Structure):

@@ -101,11 +101,11 @@ def pwpw_candidates(model: dict, probe, dtype: str, batch: int):
     out = []
     for a, b in model["edges"]:
         la, lb = kinds[a], kinds[b]
-        if la["kind"] != "pw" or lb["kind"] != "pw":
-            continue
+        if la["kind"] != "pw" or lb["kind"] != "pw" or la.get("extra_consumers", 0) or la.get("residual", 0):
+            continue  # a shortcut reads a's output (it must reach HBM) / T would carry a residual
         m = batch * la["h"] * la["w"]
         cin, cmid, cout = la["c_in"], la["c_out"], lb["c_out"]
-        dram = esize * (m * (cin + cout) + cin * cmid + cmid * cout)
+        dram = esize * (m * (cin + cout * (1 + lb.get("residual", 0))) + cin * cmid + cmid * cout)
         out.append({"op": "pwpw", "kind": "pwpw", "layers": [a, b], "tile": None, "dram_bytes": dram, "l2_bytes": dram,
                     "lbl_dram_bytes": dram + 2 * esize * m * cmid, "pred_us": 0.0,
                     "macs": m * (cin * cmid + cmid * cout)})
@@ -127,6 +127,7 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
         cin = l0["c"] if l0["kind"] == "dw" else l0["c_in"]
         src = torch.zeros((batch, l0["h"], l0["w"], cin), dtype=probe.x.dtype, device=device)
         out = torch.empty(probe._out_shape(lids[-1]), dtype=probe.x.dtype, device=device)
+        res = torch.zeros_like(out) if "residual_from" in probe.layers[lids[-1]] and dtype != "s8" else None
         tiles = [c.get("tile")]
         if tile_search and c["op"] == "dwpw" and c.get("tile"):
             d = probe.layers[lids[0]]
@@ -143,7 +144,7 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
         best = None
         for t in tiles:
             ct = dict(c, tile=t) if t is not None else c
-            f = probe._make_call(ct, src, out)
+            f = probe._make_call(ct, src, out, res)
             try:
                 us = _time(f, reps)
             except Exception as e:  # infeasible tile etc.: never chosen
@@ -156,7 +157,7 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
             meas[tuple(lids)] = best[0]
             if best[1] is not None:
                 c["tile"] = best[1]
-        del src, out
+        del src, out, res
     lbl = {l: meas[(l,)] for l in order}
     fcm_cost = {k: v for k, v in meas.items() if len(k) == 2 and v < lbl[k[0]] + lbl[k[1]]}
     sel, total = chain_dp(order, lbl, fcm_cost)

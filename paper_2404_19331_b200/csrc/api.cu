@@ -137,14 +137,34 @@ int check_epi(const fcm_epilogue* e, int dt, const char* name) {
     if (e->qmin > e->qmax || e->qmin < -128 || e->qmax > 127)
       return set_error(FCM_E_INVAL, std::string(name) + ": qmin/qmax must lie in [-128,127]");
     if (e->zp_in != 0) return set_error(FCM_E_UNSUPPORTED, std::string(name) + ": GPU paths need zp_in == 0");
-  } else if (e->act < FCM_ACT_NONE || e->act > FCM_ACT_RELU6) {
+    if (e->residual) return set_error(FCM_E_UNSUPPORTED, std::string(name) + ": int8 residual add");
+  } else if (e->act < FCM_ACT_NONE || e->act > FCM_ACT_GELU) {
     return set_error(FCM_E_INVAL, std::string(name) + ": bad activation");
   }
   return FCM_OK;
 }
 
+// an epilogue that may not carry a residual (it does not write the call's output through a PW)
+int no_residual(const fcm_epilogue* e, const char* name) {
+  return e && e->residual ? set_error(FCM_E_UNSUPPORTED, std::string(name) + ": residual add only on a PW output epilogue")
+                          : FCM_OK;
+}
+
+// residual: 16-byte aligned (vector loads) and not overlapping the output
+int check_residual(const fcm_epilogue* e, const fcm_tensor* y, const char* name) {
+  if (!e || !e->residual) return FCM_OK;
+  if (reinterpret_cast<uintptr_t>(e->residual) % 16)
+    return set_error(FCM_E_ALIGN, std::string(name) + ": residual not 16-byte aligned");
+  const char* r0 = static_cast<const char*>(e->residual);
+  const char* y0 = static_cast<const char*>(y->data);
+  const size_t nb = tensor_bytes(y);
+  if (r0 < y0 + nb && y0 < r0 + nb) return set_error(FCM_E_INVAL, std::string(name) + ": residual overlaps the output");
+  return FCM_OK;
+}
+
 Epi to_epi(const fcm_epilogue* e) {
-  return Epi{e->act, e->scale, e->bias, e->bias_q, e->mult_q, e->shift_q, e->zp_in, e->zp_out, e->qmin, e->qmax};
+  return Epi{e->act, e->scale, e->bias, e->bias_q, e->mult_q, e->shift_q, e->zp_in, e->zp_out, e->qmin, e->qmax,
+             e->residual};
 }
 
 // floor((in + p0 + p1 - k) / s) + 1; a window that does not fit the padded input gives 0 (-> the
@@ -203,6 +223,7 @@ int fcm_dw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const
   if (!w_dw) return set_error(FCM_E_INVAL, "w_dw is NULL");
   if (x->dtype != y->dtype || x->layout != y->layout) return set_error(FCM_E_INVAL, "x/y dtype or layout differ");
   FCM_TRY(check_epi(ep, x->dtype, "ep"));
+  FCM_TRY(no_residual(ep, "ep"));
   const int Ho = out_dim(x->h, geom->k, geom->stride, geom->pad_t, geom->pad_b);
   const int Wo = out_dim(x->w, geom->k, geom->stride, geom->pad_l, geom->pad_r);
   if (Ho < 1 || Wo < 1) return set_error(FCM_E_INVAL, "dw: empty output");
@@ -231,6 +252,7 @@ int fcm_pw(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep,
   if (!w_pw_packed) return set_error(FCM_E_INVAL, "w_pw is NULL");
   if (x->dtype != y->dtype) return set_error(FCM_E_INVAL, "x/y dtype differ");
   FCM_TRY(check_epi(ep, x->dtype, "ep"));
+  FCM_TRY(check_residual(ep, y, "ep"));
   if (y->n != x->n || y->h != x->h || y->w != x->w) return set_error(FCM_E_INVAL, "pw: y spatial dims mismatch");
   if (overlaps(x, y)) return set_error(FCM_E_INVAL, "pw: x and y overlap");
   const int M = x->n * x->h * x->w;
@@ -249,6 +271,8 @@ int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, con
   if (x->dtype != y->dtype) return set_error(FCM_E_INVAL, "x/y dtype differ");
   FCM_TRY(check_epi(ep_dw, x->dtype, "ep_dw"));
   FCM_TRY(check_epi(ep_pw, x->dtype, "ep_pw"));
+  FCM_TRY(no_residual(ep_dw, "ep_dw"));
+  FCM_TRY(check_residual(ep_pw, y, "ep_pw"));
   if (x->dtype == FCM_S8 && ep_pw->zp_in != ep_dw->zp_out)
     return set_error(FCM_E_INVAL, "dwpw: ep_pw.zp_in must equal ep_dw.zp_out (T's zero point)");
   const int Ho = out_dim(x->h, geom->k, geom->stride, geom->pad_t, geom->pad_b);
@@ -281,6 +305,8 @@ int fcm_pwpw(const fcm_tensor* x, const void* w1_packed, int32_t c_mid, const fc
   if (c_mid < 1) return set_error(FCM_E_INVAL, "pwpw: c_mid < 1");
   FCM_TRY(check_epi(ep1, x->dtype, "ep1"));
   FCM_TRY(check_epi(ep2, x->dtype, "ep2"));
+  FCM_TRY(no_residual(ep1, "ep1"));
+  FCM_TRY(check_residual(ep2, y, "ep2"));
   if (x->dtype == FCM_S8 && ep2->zp_in != ep1->zp_out)
     return set_error(FCM_E_INVAL, "pwpw: ep2.zp_in must equal ep1.zp_out (T's zero point)");
   if (y->n != x->n || y->h != x->h || y->w != x->w) return set_error(FCM_E_INVAL, "pwpw: y spatial dims mismatch");
@@ -303,6 +329,8 @@ int fcm_pwdw_r(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue*
   if (x->dtype == FCM_S8 && ep_dw && ep_dw->zp_in != ep_pw->zp_out)
     return set_error(FCM_E_INVAL, "pwdw_r: ep_dw.zp_in must equal ep_pw.zp_out (T's zero point)");
   FCM_TRY(check_epi(ep_dw, x->dtype, "ep_dw"));
+  FCM_TRY(no_residual(ep_pw, "ep_pw"));
+  FCM_TRY(no_residual(ep_dw, "ep_dw"));
   const int Ho = out_dim(x->h, geom->k, geom->stride, geom->pad_t, geom->pad_b);
   const int Wo = out_dim(x->w, geom->k, geom->stride, geom->pad_l, geom->pad_r);
   if (Ho < 1 || Wo < 1) return set_error(FCM_E_INVAL, "pwdw_r: empty output");

@@ -20,6 +20,7 @@ struct Epi {
   const int32_t* mult_q;
   const int32_t* shift_q;
   int zp_in, zp_out, qmin, qmax;
+  const void* residual;  // optional: same shape / dtype as the output, added after the activation
 };
 
 // ---------------------------------------------------------------------------- dtype traits
@@ -66,7 +67,37 @@ template <> struct Tr<FCM_S8> {
 // Activation as a clamp [lo, hi] (NONE: (-inf, inf), RELU: [0, inf), RELU6: [0, 6]); branch-free.
 __device__ __forceinline__ float act_lo(int act) { return act == FCM_ACT_NONE ? -INFINITY : 0.f; }
 __device__ __forceinline__ float act_hi(int act) { return act == FCM_ACT_RELU6 ? 6.f : INFINITY; }
-__device__ __forceinline__ float act_f(float v, int act) { return fminf(fmaxf(v, act_lo(act)), act_hi(act)); }
+// SiLU v * sigmoid(v) = v / (1 + e^-v) (fast exp; e^-v -> inf gives -0) and the exact (erf) GELU.
+__device__ __forceinline__ float silu_f(float v) {
+  float e, r;  // 2^(-v log2 e) and the approximate reciprocal (2 MUFU ops; rcp(inf) = 0 -> -0)
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * v));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
+  return v * r;
+}
+__device__ __forceinline__ float gelu_f(float v) { return 0.5f * v * (1.f + erff(v * 0.70710678118654752f)); }
+__device__ __forceinline__ float act_f(float v, int act) {
+  if (act == FCM_ACT_SILU) return silu_f(v);
+  if (act == FCM_ACT_GELU) return gelu_f(v);
+  return fminf(fmaxf(v, act_lo(act)), act_hi(act));
+}
+template <int ACT>
+__device__ __forceinline__ float act_t(float v) {
+  if constexpr (ACT == FCM_ACT_SILU) return silu_f(v);
+  else if constexpr (ACT == FCM_ACT_GELU) return gelu_f(v);
+  else if constexpr (ACT == FCM_ACT_RELU6) return fminf(fmaxf(v, 0.f), 6.f);
+  else if constexpr (ACT == FCM_ACT_RELU) return fmaxf(v, 0.f);
+  else return v;
+}
+// One output element of a float path: act(acc*scale + bias) (+ residual r).
+__device__ __forceinline__ float epi_fr(float a, float sc, float bi, int act, float r) { return act_f(fmaf(a, sc, bi), act) + r; }
+// Residual element i of a float-dtype tensor as fp32.
+template <int DT>
+__device__ __forceinline__ float res_at(const void* r, size_t i) {
+  if constexpr (DT == FCM_F32) return __ldg(static_cast<const float*>(r) + i);
+  else if constexpr (DT == FCM_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(r)[i]);
+  else if constexpr (DT == FCM_F16) return __half2float(static_cast<const __half*>(r)[i]);
+  else return 0.f;
+}
 
 // Per-channel epilogue constants held in registers.
 struct EpiC {
@@ -607,6 +638,8 @@ template <class F>
 __device__ __forceinline__ void with_act(int act, F&& f) {
   if (act == FCM_ACT_RELU6) f(std::integral_constant<int, 2>());
   else if (act == FCM_ACT_RELU) f(std::integral_constant<int, 1>());
+  else if (act == FCM_ACT_SILU) f(std::integral_constant<int, 3>());
+  else if (act == FCM_ACT_GELU) f(std::integral_constant<int, 4>());
   else f(std::integral_constant<int, 0>());
 }
 
@@ -616,7 +649,12 @@ __device__ __forceinline__ uint32_t epi_act2(float lo, float hi, uint64_t sc2, u
   float a, b;
   f2_unpack(f2_fma(f2_pack(lo, hi), sc2, bi2), a, b);
   uint32_t h;
-  if constexpr (DT == FCM_BF16) {
+  if constexpr (ACT >= FCM_ACT_SILU) {  // SiLU / GELU in fp32, then one rounding
+    a = act_t<ACT>(a);
+    b = act_t<ACT>(b);
+    if constexpr (DT == FCM_BF16) asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+    else asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
+  } else if constexpr (DT == FCM_BF16) {
     if constexpr (ACT == 0) asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
     else asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));
     if constexpr (ACT == 2) asm("min.bf16x2 %0, %0, %1;" : "+r"(h) : "r"(hi_c));

@@ -88,24 +88,30 @@ __global__ void __launch_bounds__(128) dw_nhwc_kernel(const __grid_constant__ CU
     load_dw_weights_h<K>(W2, wdw, C, cval ? cl : C);
     const uint64_t sc2 = f2_pack(cval ? (ep.scale ? ep.scale[cl] : 1.f) : 0.f, cval ? (ep.scale ? ep.scale[cl + 1] : 1.f) : 0.f);
     const uint64_t bi2 = f2_pack(cval && ep.bias ? ep.bias[cl] : 0.f, cval && ep.bias ? ep.bias[cl + 1] : 0.f);
-    const uint32_t lo_c = bound2<DT>(act_lo(ep.act)), hi_c = bound2<DT>(act_hi(ep.act));
+    const uint32_t hi_c = bound2<DT>(act_hi(ep.act));
     wait_x();
     const int nseg = (nrows + kSeg - 1) / kSeg;
     const int ncolg = (tw + npix - 1) / npix;
-    for (int item = warp; item < ncolg * nseg; item += 4) {
-      const int cg = item / nseg, seg = item - cg * nseg;
-      const int col = cg * npix + grp;
-      const int x = x0 + col;
-      const bool live = col < tw && x < Wo && cval;
-      const int ys = seg * kSeg;
-      const uint32_t src = smem_u32(xs) + (((live ? col : 0) * S) * pwd + wd) * 4;
-      uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + (live ? x : 0)) * C + cl) / V;
-      const size_t rstride = (size_t)Wo * C / V;
-      const int nvalid = live ? nrows - ys : 0;
-      dw_segh<DT, K, S, kSeg>(src, pb, tw_in * pb, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
-        if (r < nvalid) dst[r * rstride] = epi2_pack<DT>(acc, sc2, bi2, lo_c, hi_c);
-      });
-    }
+    // same epilogue as the fused kernels' DW stage (epi_act2): LBL and fused DW are bit-identical
+    with_act(ep.act, [&](auto actc) {
+      constexpr int ACT = decltype(actc)::value;
+      for (int item = warp; item < ncolg * nseg; item += 4) {
+        const int cg = item / nseg, seg = item - cg * nseg;
+        const int col = cg * npix + grp;
+        const int x = x0 + col;
+        const bool live = col < tw && x < Wo && cval;
+        const int ys = seg * kSeg;
+        const uint32_t src = smem_u32(xs) + (((live ? col : 0) * S) * pwd + wd) * 4;
+        uint32_t* dst = yw + (((static_cast<size_t>(n) * Ho + (y0 + ys)) * Wo + (live ? x : 0)) * C + cl) / V;
+        const size_t rstride = (size_t)Wo * C / V;
+        const int nvalid = live ? nrows - ys : 0;
+        dw_segh<DT, K, S, kSeg>(src, pb, tw_in * pb, ys, th_in - 1, W2, [&](int r, uint64_t acc) {
+          float lo, hi;
+          f2_unpack(acc, lo, hi);
+          if (r < nvalid) dst[r * rstride] = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
+        });
+      }
+    });
     return;
   } else if constexpr (DT == FCM_S8 && K == 3) {
     // int8 column-pair FFMA2 core (exact, see dw3_pair_i8); a lane owns one word (4 channels) of

@@ -35,6 +35,8 @@ static ll cdiv(ll a, ll b) { return (a + b - 1) / b; }
 struct Layer {
   std::string id, kind;
   ll H, W, C, Cout, k = 1, s = 1, pt = 0, pl = 0, pb = 0, pr = 0, Ho, Wo;
+  ll res = 0;        // 1: the output epilogue adds a residual (shortcut) of the output's shape
+  ll extra_out = 0;  // consumers outside the edge list (a residual shortcut reads this output)
 };
 
 struct Gpu {
@@ -283,7 +285,7 @@ static Cost b200_pw(const Layer& p, ll N, int dt, ll b, const Gpu& gp) {
   c.th = bm; c.nsplit = cdiv(p.Cout, bn);
   const Units u = pw_units(M, p.C, p.Cout, bm, bn);
   c.l2 = u.total() * b;
-  c.dram = (M * (p.C + p.Cout) + p.C * p.Cout) * b;
+  c.dram = (M * (p.C + p.Cout + p.res * p.Cout) + p.C * p.Cout) * b;
   c.pw_macs = M * p.C * p.Cout;
   c.us = t_us(c, dt, gp);
   return c;
@@ -308,7 +310,7 @@ static Cost b200_dwpw(const Layer& d, const Layer& p, ll N, int dt, ll b, const 
   c.nb = g.nb; c.th = g.th; c.tw = g.tw; c.nsplit = cdiv(Co, bn);
   const Units u = units("dwpw", N, d, d.C, Co, g.nb, g.th, g.tw, bn);
   c.l2 = u.total() * b;
-  c.dram = (N * (d.H * d.W * d.C + d.Ho * d.Wo * Co) + d.k * d.k * d.C + d.C * Co) * b;
+  c.dram = (N * (d.H * d.W * d.C + d.Ho * d.Wo * Co * (1 + p.res)) + d.k * d.k * d.C + d.C * Co) * b;
   c.dw_macs = N * d.Ho * d.Wo * d.C * d.k * d.k * c.nsplit;
   c.pw_macs = N * d.Ho * d.Wo * d.C * Co;
   c.us = t_us(c, dt, gp);
@@ -372,6 +374,8 @@ static Layer parse_layer(const Value& v) {
   Layer l;
   l.id = v.str("id", "");
   l.kind = v.str("kind", "");
+  l.res = geti(v, "residual", 0) != 0;
+  l.extra_out = geti(v, "extra_consumers", 0);
   l.H = geti(v, "h", 0);
   l.W = geti(v, "w", 0);
   if (l.kind == "dw") {
@@ -440,6 +444,7 @@ static std::string run(const char* model_json, const char* gpu_json) {
   const size_t n = L.size();
   // edges -> producer/consumer counts; default: a chain in list order
   std::vector<int> outdeg(n, 0), indeg(n, 0);
+  for (size_t i = 0; i < n; ++i) outdeg[i] = (int)L[i].extra_out;  // residual shortcuts (single-consumer rule)
   std::vector<char> link(n, 0);  // link[i]: edge L[i-1] -> L[i]
   const Value* ev = m.get("edges");
   auto idx = [&](const std::string& id) -> int {
@@ -503,7 +508,7 @@ static std::string run(const char* model_json, const char* gpu_json) {
         f = b200_dwpw(a, c, N, dt, b, gp);
         f.exec = f.ok && k_ok;
         f.ok = true;
-        f.dram = (N * (a.H * a.W * a.C + a.Ho * a.Wo * c.Cout) + a.k * a.k * a.C + a.C * c.Cout) * b;
+        f.dram = (N * (a.H * a.W * a.C + a.Ho * a.Wo * c.Cout * (1 + c.res)) + a.k * a.k * a.C + a.C * c.Cout) * b;
         f.gma = bst.gma * b; f.p_th = bst.th; f.p_tw = bst.tw; f.p_td = bst.td;
       } else {
         f = b200_dwpw(a, c, N, dt, b, gp);

@@ -6,6 +6,8 @@
 //    EfficientNet-B0), which TMA cannot address.
 // Same structure as the tensor-core FCMs: the intermediate T lives only in shared memory and is
 // rounded / requantised to the feature-map dtype before the second convolution.
+#include <cstdint>
+
 #include "common.cuh"
 #include "host.h"
 
@@ -26,13 +28,20 @@ __device__ __forceinline__ typename Tr<DT>::acc_t mac(typename Tr<DT>::acc_t a, 
   else return fmaf(a, b, c);
 }
 
-// Conv-Norm-Act of one accumulator -> storage value.
+// Conv-Norm-Act of one accumulator -> storage value; `oidx` = the element's index in the output
+// (for the optional residual, float paths; SIZE_MAX on intermediate T writes).
 template <int DT>
-__device__ __forceinline__ typename Tr<DT>::T epi1(typename Tr<DT>::acc_t a, const EpiC& c, const Epi& e) {
-  if constexpr (DT == FCM_S8) return static_cast<int8_t>(requant_i8(a, c, e.zp_out, e.qmin, e.qmax));
-  else if constexpr (DT == FCM_F32) return epi_f(a, c.sc, c.bi, e.act);
-  else if constexpr (DT == FCM_BF16) return __float2bfloat16_rn(epi_f(a, c.sc, c.bi, e.act));
-  else return __float2half_rn(epi_f(a, c.sc, c.bi, e.act));
+__device__ __forceinline__ typename Tr<DT>::T epi1(typename Tr<DT>::acc_t a, const EpiC& c, const Epi& e,
+                                                   size_t oidx = SIZE_MAX) {
+  if constexpr (DT == FCM_S8) {
+    return static_cast<int8_t>(requant_i8(a, c, e.zp_out, e.qmin, e.qmax));
+  } else {
+    const float r = (e.residual && oidx != SIZE_MAX) ? res_at<DT>(e.residual, oidx) : 0.f;
+    const float v = epi_fr(a, c.sc, c.bi, e.act, r);
+    if constexpr (DT == FCM_F32) return v;
+    else if constexpr (DT == FCM_BF16) return __float2bfloat16_rn(v);
+    else return __float2half_rn(v);
+  }
 }
 
 // ------------------------------------------------------------------ LBL PW
@@ -181,7 +190,7 @@ __global__ void __launch_bounds__(256) pw_simt_kernel(const typename Tr<DT>::T* 
       if (m >= M) continue;
       TT v[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = epi1<DT>(acc[i][j], c[j], ep);
+      for (int j = 0; j < 4; ++j) v[j] = epi1<DT>(acc[i][j], c[j], ep, (size_t)m * N + nb + j);
       store4<DT>(y + (size_t)m * N + nb, v);
     }
   } else {
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(256) pw_simt_kernel(const typename Tr<DT>::T* 
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int m = m0 + ty * 4 + i;
-        if (m < M) y[(size_t)m * N + n] = epi1<DT>(acc[i][j], c, ep);
+        if (m < M) y[(size_t)m * N + n] = epi1<DT>(acc[i][j], c, ep, (size_t)m * N + n);
       }
     }
   }
@@ -296,7 +305,10 @@ __global__ void __launch_bounds__(256) dwpw_simt_kernel(const typename Tr<DT>::T
     for (int i = 0; i < 4; ++i) {
       const int p = ty * 4 + i;
       const int yo = tyi * 8 + p / 8, xo = txi * 8 + p % 8;
-      if (yo < Ho && xo < Wo) y[(((size_t)n * Ho + yo) * Wo + xo) * Cout + co] = epi1<DT>(acc[i][j], c, ep);
+      if (yo < Ho && xo < Wo) {
+        const size_t o = (((size_t)n * Ho + yo) * Wo + xo) * Cout + co;
+        y[o] = epi1<DT>(acc[i][j], c, ep, o);
+      }
     }
   }
 }

@@ -48,8 +48,17 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // Epilogue of 16 accumulator columns [n_base, n_base+16) of one row -> packed storage words.
 // Constants come from smem as 128-bit broadcast loads (n_base is a multiple of 16).
 template <int DT>
+__device__ __forceinline__ float2 word2f(uint32_t w) {
+  if constexpr (DT == FCM_BF16) return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  else return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+
+// Epilogue of 16 accumulator columns [n_base, n_base+16) of one row -> packed storage words.
+// Constants come from smem as 128-bit broadcast loads (n_base is a multiple of 16). rw (bf16 / f16
+// only): the 8 packed words of the residual (shortcut) for these 16 columns, or nullptr.
+template <int DT>
 __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
-                                      uint32_t (&out)[8]) {
+                                      uint32_t (&out)[8], const uint32_t* rw = nullptr) {
   if constexpr (DT == FCM_S8) {
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -67,6 +76,31 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
       out[w] = word;
     }
   } else {
+    if (rw || e.act > FCM_ACT_RELU6) {
+      // SiLU / GELU and / or the residual: 4 columns at a time (registers);
+      // the activation is dispatched once per call, so only one variant's code is fetched (the
+      // DWPW epilogue shares the SM's instruction cache with the DW stage's hot loop)
+      with_act(e.act, [&](auto actc) {
+        constexpr int ACT = decltype(actc)::value;
+        // GELU's erf is ~30 instructions: keep its loop rolled (instruction-cache footprint)
+#pragma unroll(ACT == FCM_ACT_GELU ? 1 : 4)
+        for (int q = 0; q < 4; ++q) {
+          const uint4 a = lds128(cs.base + 4 * (n_base + 4 * q));
+          const uint4 b = lds128(cs.base + 4 * (cs.ncap + n_base + 4 * q));
+          float v0 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q]), __uint_as_float(a.x), __uint_as_float(b.x)));
+          float v1 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q + 1]), __uint_as_float(a.y), __uint_as_float(b.y)));
+          float v2 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q + 2]), __uint_as_float(a.z), __uint_as_float(b.z)));
+          float v3 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q + 3]), __uint_as_float(a.w), __uint_as_float(b.w)));
+          if (rw) {
+            const float2 s0 = word2f<DT>(rw[2 * q]), s1 = word2f<DT>(rw[2 * q + 1]);
+            v0 += s0.x; v1 += s0.y; v2 += s1.x; v3 += s1.y;
+          }
+          out[2 * q] = pack2<DT, false>(v0, v1);
+          out[2 * q + 1] = pack2<DT, false>(v2, v3);
+        }
+      });
+      return;
+    }
     float sc[16], bi[16];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -89,6 +123,26 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
         out[w] = pack2<DT, true>(fminf(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]), hi_c),
                                  fminf(fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]), hi_c));
     }
+  }
+}
+
+// Residual (shortcut) words of 32 consecutive bf16 / f16 output columns, loaded one 32-column
+// chunk ahead of their use so the epilogue never waits a global round trip.
+struct Res32 {
+  uint4 v[4];
+};
+__device__ __forceinline__ uint4 ldg_nc128(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+// columns [col, col + 32) of the row at element offset `rowoff`; 8-column pieces at or past
+// `lim` (the row's valid width) and rows with !ok read as 0
+__device__ __forceinline__ void res32_load(const void* r, size_t rowoff, int col, int lim, bool ok, Res32& o) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    o.v[p] = make_uint4(0u, 0u, 0u, 0u);
+    if (ok && col + 8 * p < lim) o.v[p] = ldg_nc128(static_cast<const uint16_t*>(r) + rowoff + col + 8 * p);
   }
 }
 
@@ -143,13 +197,18 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tacc, int BN, int n0, int
 // 128-byte column chunks hs, hs + G, ... ; it converts its 32 x CPC block into a private SW128
 // staging buffer (4 KB) and its lane 0 issues the TMA store of a (CPC x 32-row) box -- no
 // CTA-wide barriers in the epilogue.
+// row0 / M: global output row of TMEM lane 0 and the row count (for the optional residual).
 template <int DT, class StoreFn>
 __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0, int N, const EpiS& cs, const Epi& e,
-                                                   uint8_t* wstage, int& sbuf, int hs, int G, StoreFn&& store) {
+                                                   uint8_t* wstage, int& sbuf, int hs, int G, long row0, int M,
+                                                   StoreFn&& store) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int CPC = 128 / ES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3;
+  const long grow = row0 + q * 32 + lane;
+  const bool hasres = ES == 2 && e.residual != nullptr;
+  const bool rrow = hasres && grow < M;
   const int valid = min(BN, N - n0);
   const int nch = (valid + CPC - 1) / CPC;
   for (int cc = hs; cc < nch; cc += G, ++sbuf) {
@@ -160,6 +219,30 @@ __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0
     for (int c32 = 0; c32 < CPC; c32 += 32) {
       const int c0 = cc * CPC + c32;
       if (c0 >= BN) break;
+      if (ES == 2 && (hasres || e.act > FCM_ACT_RELU6)) {
+        // SiLU / GELU / residual: 16 columns per TMEM load, the residual words
+        // issued before it (register budget 18 warps x 96; the 16 epilogue warps hide the latency)
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          uint4 rw[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+          const int col = n0 + c0 + 16 * hh;
+          if (hasres) {
+            const uint16_t* rp = static_cast<const uint16_t*>(e.residual) + (size_t)grow * N + col;
+            if (rrow && col < N) rw[0] = ldg_nc128(rp);
+            if (rrow && col + 8 < N) rw[1] = ldg_nc128(rp + 8);
+          }
+          uint32_t r[16];
+          tmem_ld16(tacc + ((uint32_t)(q * 32) << 16) + c0 + 16 * hh, r);
+          tmem_ld_wait();
+          uint32_t o[8];
+          epi16<DT>(r, cs, e, col, o, hasres ? reinterpret_cast<const uint32_t*>(rw) : nullptr);
+          const int vi0 = (c32 + 16 * hh) * ES / 16;
+#pragma unroll
+          for (int v = 0; v < ES; ++v)
+            sts128(smem_u32(buf) + sw128_vec(lane, vi0 + v), o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+        }
+        continue;
+      }
       uint32_t r[32];
       tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + c0, r);
       tmem_ld_wait();
@@ -308,7 +391,7 @@ __global__ void __launch_bounds__(576, 1)
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
       if (!(dbg & 32))
-        epilogue_tile_warp<DT>(tbase + acc * BN, BN, n0, N, cs, ep, stage + warp * 4096, sbuf, hs, spg,
+        epilogue_tile_warp<DT>(tbase + acc * BN, BN, n0, N, cs, ep, stage + warp * 4096, sbuf, hs, spg, m0, M,
                                [&](const uint8_t* buf, int c, int r) {
                                  if (!(dbg & 16)) tma_store_2d(&tmy, buf, c, m0 + r);
                                });
@@ -749,19 +832,39 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
       int ns, nbi, tyi, txi;
       decode(t, ns, nbi, tyi, txi);
       const int valid = min(BN, Cout - ns * BN);
-      group_wait(tfull + acc, rt.ph, warp == 0, 4, 128);
-      if (threadIdx.x == 0) stamp(local, 3);
-      tc_fence_after();
-      for (int h = 0; h < MB && !(dbg & 2); ++h) {
+      // the <= 2 output pixels of this lane (row blocks h): NHWC offsets and validity
+      size_t po0, po1;
+      bool pok0, pok1;
+      auto pix = [&](int h, size_t& po, bool& pok) {
         const int m = h * 128 + q * 32 + lane;
         const int b = fdiv(m, dv.thw), rem = m - b * (th * tw);
         const int yy = fdiv(rem, dv.tw), xx = rem - yy * tw;
         const int n = nbi * nb + b, yo = tyi * th + yy, xo = txi * tw + xx;
-        const bool ok = m < tpx && n < N && yo < Ho && xo < Wo;
-        uint8_t* dst = yb + ((((size_t)n * Ho + yo) * Wo + xo) * Cout + (size_t)ns * BN) * ES;
+        pok = h < MB && m < tpx && n < N && yo < Ho && xo < Wo;
+        po = pok ? (((size_t)n * Ho + yo) * Wo + xo) * Cout + (size_t)ns * BN : 0;
+      };
+      pix(0, po0, pok0);
+      pix(1, po1, pok1);
+      // residual (shortcut) words one 32-column step ahead; the first step's before the TMEM wait
+      const bool hasres = ES == 2 && ep.residual != nullptr;
+      Res32 rnext;
+      if (hasres) res32_load(ep.residual, po0, 0, valid, pok0, rnext);
+      group_wait(tfull + acc, rt.ph, warp == 0, 4, 128);
+      if (threadIdx.x == 0) stamp(local, 3);
+      tc_fence_after();
+      for (int h = 0; h < MB && !(dbg & 2); ++h) {
+        const bool ok = h ? pok1 : pok0;
+        const size_t poh = h ? po1 : po0;
+        uint8_t* dst = yb + poh * ES;
         const uint32_t tq = tbase + acc * (MB * BN) + h * BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
         for (int c0 = 0; c0 < valid; c0 += 32) {
+          Res32 rcur;
+          if (hasres) {
+            rcur = rnext;
+            if (c0 + 32 < valid) res32_load(ep.residual, poh, c0 + 32, valid, ok, rnext);
+            else if (h + 1 < MB) res32_load(ep.residual, po1, 0, valid, pok1, rnext);
+          }
           uint32_t r[32];
           tmem_ld32(tq + c0, r);
           tmem_ld_wait();
@@ -770,7 +873,15 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             const int cb = c0 + 16 * hh;  // 16 columns = 2 x 8-column (16 B bf16 / 8 B int8) pieces
             if (cb >= valid) break;
             uint32_t o[8];
-            epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o);
+            if constexpr (ES == 2) {
+              if (hasres) {  // the shortcut input at the same NHWC position
+                epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o, reinterpret_cast<const uint32_t*>(&rcur.v[2 * hh]));
+              } else {
+                epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o);
+              }
+            } else {
+              epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o);
+            }
             if (ok) {
               if constexpr (ES == 2) {
                 stg128(dst + cb * 2, o[0], o[1], o[2], o[3]);
@@ -1656,6 +1767,7 @@ __global__ void __launch_bounds__(608, 1)
         group_wait(acc2full + ra.i, ra.ph, warp == 4, 3, 12 * 32);
         tc_fence_after();
         epilogue_tile_warp<DT>(tacc2 + ra.i * BN2, BN2, j * BN2, N, cs2, ep2, stage + w2i * 4096, sbuf, hs, 3,
+                               (long)t * 128, M,
                                [&](const uint8_t* buf, int c, int rr) { tma_store_2d(&tmy, buf, c, t * 128 + rr); });
         tc_fence_before();
         __syncwarp();

@@ -9,6 +9,8 @@ image index so that batch shards are exact slices of one global batch.
 """
 from __future__ import annotations
 
+import dataclasses
+
 import numpy as np
 import torch
 
@@ -20,8 +22,11 @@ TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16, 
 ESIZE = {"f32": 4, "bf16": 2, "f16": 2, "s8": 1}
 
 
-def model_json(net: str, dtype: str, batch: int, mode: str = "b200") -> dict:
-    """Planner input for a named network: the layer list plus producer->consumer edges."""
+def model_json(net: str, dtype: str, batch: int, mode: str = "b200", shortcuts: bool = True) -> dict:
+    """Planner input for a named network: the layer list plus producer->consumer edges.
+    shortcuts=False drops the residual adds (the paper's DW/PW-only model, SURVEY App. A byte pins);
+    int8 stacks never carry them (no int8 residual epilogue, reading R1b)."""
+    shortcuts = shortcuts and dtype != "s8"
     blocks = NETWORKS[net]()
     ids = layer_ids(blocks)
     out = []
@@ -33,11 +38,22 @@ def model_json(net: str, dtype: str, batch: int, mode: str = "b200") -> dict:
         else:
             out.append({"id": lid, "kind": "pw", "h": l["h"], "w": l["w"], "c_in": l["c_in"],
                         "c_out": l["c_out"]})
+            if shortcuts and "residual_from" in l:
+                out[-1]["residual"] = 1  # the epilogue reads one output-shaped shortcut tensor
     edges = []
     for i in range(1, len(ids)):
         (a, ba, _), (c, bc, _) = ids[i - 1], ids[i]
         if ba == bc or block_source(net, blocks, bc)[0] == "chain":
             edges.append([a, c])
+    if shortcuts:
+        # the shortcut re-reads the producer's output: a second consumer, so that output is never an
+        # FCM intermediate (single-consumer rule, reading R20)
+        by_id = {l["id"]: l for l in out}
+        for lid, _, l in ids:
+            src = l.get("residual_from")
+            for a, c in edges if src else ():
+                if c == src:
+                    by_id[a]["extra_consumers"] = by_id[a].get("extra_consumers", 0) + 1
     return {"dtype": dtype, "batch": batch, "mode": mode, "layers": out, "edges": edges}
 
 
@@ -107,7 +123,8 @@ class Network:
     def _build_steps(self):
         cur = self.x
         stage_in = {}
-        self.outputs, self.inputs, self.entries = [], [], []
+        entry_in = {}  # first layer of an entry -> its input tensor (shortcut sources)
+        self.outputs, self.inputs, self.entries, self.residuals = [], [], [], []
         for e in self._entries():
             lids = e["layers"]
             l0 = self.layers[lids[0]]
@@ -123,7 +140,13 @@ class Network:
                             self.net, self.dtype, role, self.n0, self.batch, l0["h"], l0["w"], c, self.seed).to(self.dev)
                     src = stage_in[role]
             out = torch.empty(self._out_shape(lids[-1]), dtype=TORCH_DT[self.dtype], device=self.dev)
-            self.steps.append(self._make_call(e, src, out))
+            entry_in[lids[0]] = src
+            rf = self.layers[lids[-1]].get("residual_from") if self.dtype != "s8" else None
+            if rf is not None and rf not in entry_in:
+                raise ValueError(f"plan hides the shortcut source {rf} of {lids[-1]} inside a fused entry")
+            res = entry_in[rf] if rf is not None else None
+            self.steps.append(self._make_call(e, src, out, res))
+            self.residuals.append(res)
             self.step_info.append(dict(e, in_shape=tuple(src.shape), out_shape=tuple(out.shape)))
             cur = out
             self.outputs.append(out)
@@ -131,21 +154,27 @@ class Network:
             self.entries.append(e)
         self.out = cur
 
-    def _make_call(self, e, src, out):
+    def _make_call(self, e, src, out, res=None):
+        """One libfcm call for plan entry e; `res` = the shortcut tensor added by the entry's output
+        epilogue, or None."""
         op, lids, tile = e["op"], e["layers"], e.get("tile")
+        withres = (lambda ep: ep) if res is None else (lambda ep: dataclasses.replace(ep, residual=res))
         if op == "dw":
             l = self.layers[lids[0]]
             w, ep = self.params[lids[0]]
             return lambda: fcm.dw(src, w, l["stride"], None, ep, out=out, tile=tile)
         if op == "pw":
             w, ep = self.params[lids[0]]
+            ep = withres(ep)
             return lambda: fcm.pw(src, w, ep, out=out)
         if op == "dwpw":
             l = self.layers[lids[0]]
             (wd, ed), (wp, ep) = self.params[lids[0]], self.params[lids[1]]
+            ep = withres(ep)
             return lambda: fcm.dwpw(src, wd, l["stride"], None, ed, wp, ep, out=out, tile=tile)
         if op == "pwpw":
             (w1, e1), (w2, e2) = self.params[lids[0]], self.params[lids[1]]
+            e2 = withres(e2)
             return lambda: fcm.pwpw(src, w1, e1, w2, e2, out=out)
         if op == "pwdw_r":
             l = self.layers[lids[1]]

@@ -85,7 +85,7 @@ def activations(seed: int, role: str, n0: int, n: int, h: int, w: int, c: int, k
 # ----------------------------------------------------------------------------------
 # layer parameters
 # ----------------------------------------------------------------------------------
-ACT_NONE, ACT_RELU, ACT_RELU6 = 0, 1, 2
+ACT_NONE, ACT_RELU, ACT_RELU6, ACT_SILU, ACT_GELU = 0, 1, 2, 3, 4
 INT8_RELU6_QMAX = 96  # synthetic output scale: real 6.0 <-> 96 LSB
 
 

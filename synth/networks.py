@@ -4,14 +4,18 @@ Only shapes: no arithmetic of the method. Each network is a list of *blocks*; a 
 a list of layer dicts in execution order:
 
   {"kind": "dw", "h", "w", "c", "k", "stride", "act"}      (pads are k//2 on all sides)
-  {"kind": "pw", "h", "w", "c_in", "c_out", "act"}
+  {"kind": "pw", "h", "w", "c_in", "c_out", "act"[, "residual_from": layer id]}
 
-Stem convolutions, SE, pooling and classifier heads are not DW/PW layers and are omitted
-(SURVEY §8(f) rank 4); residual adds are likewise outside the paper's model.
+"residual_from" (the inverted-residual shortcut of P:50): the PW's epilogue
+adds the INPUT of that layer (same shape as the PW's output) after its activation -- MobileNetV2 /
+EfficientNet-B0 / ProxylessNAS blocks with stride 1 and C_in == C_out, CeiT's LeFF and CMT's
+IRFFN (x + FFN(x)), Xception's middle-flow blocks. Stem convolutions, SE, pooling and classifier
+heads are not DW/PW layers and are omitted; so are shortcuts that are not identities (Xception's
+1x1 s2 projections) and CMT's DW-local shortcut (reading R24).
 """
 from __future__ import annotations
 
-from synth import ACT_NONE, ACT_RELU, ACT_RELU6
+from synth import ACT_GELU, ACT_NONE, ACT_RELU, ACT_RELU6, ACT_SILU
 
 
 def _dw(h, w, c, k, s, act=ACT_RELU6):
@@ -39,8 +43,9 @@ def mobilenet_v1():
     return blocks
 
 
-def _inverted_residuals(table, k_of=None):
-    """table rows: (t, c_out, n, s[, k]); input 112x112x32."""
+def _inverted_residuals(table, act=ACT_RELU6, bi0=0):
+    """table rows: (t, c_out, n, s[, k]); input 112x112x32. A block with stride 1 and
+    C_in == C_out adds its input to the projection output (residual_from its first layer)."""
     blocks, hw, c = [], 112, 32
     for row in table:
         t, co, n, s = row[:4]
@@ -51,16 +56,19 @@ def _inverted_residuals(table, k_of=None):
             b = []
             mid = c * t
             if t != 1:
-                b.append(_pw(hw, hw, c, mid))
-            b.append(_dw(hw, hw, mid, k, st))
+                b.append(_pw(hw, hw, c, mid, act))
+            b.append(_dw(hw, hw, mid, k, st, act))
             b.append(_pw(ho, ho, mid, co, ACT_NONE))
+            if st == 1 and c == co:
+                b[-1]["residual_from"] = f"b{bi0 + len(blocks)}.0"
             blocks.append(b)
             hw, c = ho, co
     return blocks, hw, c
 
 
 def mobilenet_v2():
-    """configs[2]: 17 inverted residuals (t=6 except block 0) + final PW 320->1280."""
+    """configs[2]: 17 inverted residuals (t=6 except block 0; 10 with the identity shortcut) +
+    final PW 320->1280."""
     blocks, hw, c = _inverted_residuals([(1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2),
                                          (6, 96, 3, 1), (6, 160, 3, 2), (6, 320, 1, 1)])
     blocks.append([_pw(hw, hw, c, 1280)])
@@ -68,11 +76,12 @@ def mobilenet_v2():
 
 
 def efficientnet_b0():
-    """configs[3]: 16 MBConv blocks (3x3 and 5x5 DW, SE omitted, RELU6) + final PW 320->1280."""
+    """configs[3]: 16 MBConv blocks (3x3 and 5x5 DW, SiLU, identity shortcuts; SE omitted) +
+    final PW 320->1280 (SiLU)."""
     blocks, hw, c = _inverted_residuals([(1, 16, 1, 1, 3), (6, 24, 2, 2, 3), (6, 40, 2, 2, 5),
                                          (6, 80, 3, 2, 3), (6, 112, 3, 1, 5), (6, 192, 4, 2, 5),
-                                         (6, 320, 1, 1, 3)])
-    blocks.append([_pw(hw, hw, c, 1280)])
+                                         (6, 320, 1, 1, 3)], act=ACT_SILU)
+    blocks.append([_pw(hw, hw, c, 1280, ACT_SILU)])
     return blocks
 
 
@@ -103,6 +112,8 @@ def proxylessnas_gpu():
             b.append(_pw(hw, hw, c, c * t))
         b.append(_dw(hw, hw, c * t, k, st))
         b.append(_pw(ho, ho, c * t, co, ACT_NONE))
+        if st == 1 and c == co:
+            b[-1]["residual_from"] = f"b{len(blocks)}.0"
         blocks.append(b)
         hw, c = ho, co
     blocks.append([_pw(hw, hw, c, 1728)])
@@ -114,29 +125,39 @@ def xception():
     (entry flow after the two stem convs, 8x3 middle flow, exit flow). A separable conv is
     DW 3x3 (no BN/activation in between) -> PW, BN, ReLU. Max-pools between entry/exit blocks and
     the 1x1 s2 residual shortcuts are not DW/PW layers (omitted); a block after a pool reads a
-    fresh map of the pooled size."""
+    fresh map of the pooled size. Each middle-flow module (3 separable convs) adds its input to
+    its output (identity shortcut: residual_from the first DW of the module)."""
     spec = [(147, 64, 128), (147, 128, 128), (74, 128, 256), (74, 256, 256), (37, 256, 728), (37, 728, 728)]
     spec += [(19, 728, 728)] * 24 + [(19, 728, 728), (19, 728, 1024), (10, 1024, 1536), (10, 1536, 2048)]
-    return [[_dw(hw, hw, ci, 3, 1, ACT_NONE), _pw(hw, hw, ci, co, ACT_RELU)] for hw, ci, co in spec]
+    blocks = [[_dw(hw, hw, ci, 3, 1, ACT_NONE), _pw(hw, hw, ci, co, ACT_RELU)] for hw, ci, co in spec]
+    for m in range(8):  # middle flow: blocks 6 + 3m .. 8 + 3m
+        blocks[8 + 3 * m][-1]["residual_from"] = f"b{6 + 3 * m}.0"
+    return blocks
 
 
 def ceit_leff():
     """the LeFF modules of CeiT-T (12 blocks on the 14x14
-    token map, C = 192, expansion 4): PW 192->768, DW 3x3, PW 768->192. GELU is read as ReLU
-    (GELU is §8(f) rank 4); attention sits between blocks, so each LeFF reads the stage map."""
-    return [[_pw(14, 14, 192, 768, ACT_RELU), _dw(14, 14, 768, 3, 1, ACT_RELU), _pw(14, 14, 768, 192, ACT_RELU)]
-            for _ in range(12)]
+    token map, C = 192, expansion 4): PW 192->768 + GELU, DW 3x3 + GELU, PW 768->192, + the
+    block's shortcut x + LeFF(x); attention sits between blocks, so each LeFF reads the stage map."""
+    blocks = []
+    for i in range(12):
+        b = [_pw(14, 14, 192, 768, ACT_GELU), _dw(14, 14, 768, 3, 1, ACT_GELU), _pw(14, 14, 768, 192, ACT_NONE)]
+        b[-1]["residual_from"] = f"b{i}.0"
+        blocks.append(b)
+    return blocks
 
 
 def cmt_irffn():
     """the IRFFN modules of CMT-S (stages 56/28/14/7 with
-    C = 64/128/256/512 and 3/3/16/3 blocks, expansion 4): PW C->4C, DW 3x3, PW 4C->C. GELU read
-    as ReLU; the DW's residual add is omitted (rank 4); each IRFFN reads its stage map."""
+    C = 64/128/256/512 and 3/3/16/3 blocks, expansion 4): PW C->4C + GELU, DW 3x3 + GELU, PW 4C->C,
+    + the block's shortcut x + IRFFN(x). The DW-local shortcut inside IRFFN is omitted (a DW
+    epilogue residual, reading R24); each IRFFN reads its stage map."""
     blocks = []
     for hw, c, n in [(56, 64, 3), (28, 128, 3), (14, 256, 16), (7, 512, 3)]:
         for _ in range(n):
-            blocks.append([_pw(hw, hw, c, 4 * c, ACT_RELU), _dw(hw, hw, 4 * c, 3, 1, ACT_RELU),
-                           _pw(hw, hw, 4 * c, c, ACT_NONE)])
+            b = [_pw(hw, hw, c, 4 * c, ACT_GELU), _dw(hw, hw, 4 * c, 3, 1, ACT_GELU), _pw(hw, hw, 4 * c, c, ACT_NONE)]
+            b[-1]["residual_from"] = f"b{len(blocks)}.0"
+            blocks.append(b)
     return blocks
 
 

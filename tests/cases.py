@@ -51,7 +51,7 @@ def layer_params(seed, name, kind, fmt, c_in, c_out=None, k=3, act=synth.ACT_REL
     return p
 
 
-def device_epi(p, fmt, dev):
+def device_epi(p, fmt, dev, residual=None):
     import paper_2404_19331_b200 as fcm
     if fmt == "s8":
         i32 = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.int32, device=dev)
@@ -59,7 +59,7 @@ def device_epi(p, fmt, dev):
                             shift_q=i32(p["shift_q"]), zp_in=p.get("zp_in", 0), zp_out=p.get("zp_out", 0),
                             qmin=p["qmin"], qmax=p["qmax"])
     f32 = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float32, device=dev)
-    return fcm.Epilogue(act=p["act"], scale=f32(p["scale"]), bias=f32(p["bias"]))
+    return fcm.Epilogue(act=p["act"], scale=f32(p["scale"]), bias=f32(p["bias"]), residual=residual)
 
 
 def make_x(seed, fmt, n, h, w, c, role="x"):
@@ -86,11 +86,17 @@ class Case:
     """One fused or unfused layer on seeded inputs, both sides."""
 
     def __init__(self, op, fmt, n, h, w, c_in, c_out=None, k=3, s=1, pads=None, seed=synth.SEED, tile=None,
-                 act_dw=synth.ACT_RELU6, act_pw=synth.ACT_NONE, c_mid=None):
+                 act_dw=synth.ACT_RELU6, act_pw=synth.ACT_NONE, c_mid=None, residual=False):
         self.op, self.fmt, self.k, self.s, self.tile = op, fmt, k, s, tile
         self.pads = (k // 2,) * 4 if pads is None else tuple(pads)
         self.x = make_x(seed, fmt, n, h, w, c_in)
         self.c_in, self.c_out = c_in, c_out
+        self.res = None  # residual (shortcut) tensor of the output's shape, SURVEY §8(f) rank 4
+        if residual:
+            pt, pl, pb, pr = self.pads
+            ho = oc.out_size(h, k, s, pt, pb) if op == "dwpw" else h
+            wo = oc.out_size(w, k, s, pl, pr) if op == "dwpw" else w
+            self.res = make_x(seed, fmt, n, ho, wo, c_out, role="residual")
         if op in ("dw",):
             self.pd = layer_params(seed, "dw", "dw", fmt, c_in, k=k, act=act_dw)
         elif op == "pw":
@@ -107,6 +113,8 @@ class Case:
             self.pp2 = layer_params(seed, "pw2", "pw", fmt, c_mid, c_out, act=act_pw)
         else:
             raise ValueError(op)
+        if self.res is not None:
+            (self.pp2 if op == "pwpw" else self.pp)["residual"] = as_np(self.res, fmt)
 
     # ------------------------------------------------------------------ oracle
     def oracle(self):
@@ -139,13 +147,14 @@ class Case:
         if hasattr(self, "pd"):
             wdw = stored(self.pd["w"], f).to(dev)
             ed = device_epi(self.pd, f, dev)
+        res = None if self.res is None else self.res.to(dev)
         if hasattr(self, "pp"):
             wpk = fcm.pack_pw(stored(self.pp["w"], f).to(dev))
-            ep = device_epi(self.pp, f, dev)
+            ep = device_epi(self.pp, f, dev, res)
         if self.op == "pwpw":
             w1 = fcm.pack_pw(stored(self.pp1["w"], f).to(dev))
             w2 = fcm.pack_pw(stored(self.pp2["w"], f).to(dev))
-            y = fcm.pwpw(x, w1, device_epi(self.pp1, f, dev), w2, device_epi(self.pp2, f, dev))
+            y = fcm.pwpw(x, w1, device_epi(self.pp1, f, dev), w2, device_epi(self.pp2, f, dev, res))
         elif self.op == "dw":
             y = fcm.dw(x, wdw, self.s, self.pads, ed, tile=self.tile)
         elif self.op == "pw":
@@ -162,9 +171,13 @@ class Case:
         return compare(self.gpu(dev), ref, mag, self.fmt, f"{self.op}/{self.fmt}")
 
 
-def oracle_entry(e, layers, prm, x, fmt):
-    """Oracle output (and R10 magnitude, None for int8) of one plan entry applied to input x."""
+def oracle_entry(e, layers, prm, x, fmt, res=None):
+    """Oracle output (and R10 magnitude, None for int8) of one plan entry applied to input x;
+    res = the shortcut tensor its output epilogue adds, or None."""
     op, lids = e["op"], e["layers"]
+    if res is not None:
+        prm = dict(prm)
+        prm[lids[-1]] = dict(prm[lids[-1]], residual=res)
     pads = lambda l: (l["k"] // 2,) * 4
     f64 = fmt != "s8"
     if op == "dw":

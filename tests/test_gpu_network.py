@@ -130,8 +130,8 @@ def test_fusion_case_networks_bf16_entries_match_oracle(net):
     torch.cuda.synchronize()
     prm = onet.params(net, "bf16")
     fused = 0
-    for e, x, y in zip(a.entries, a.inputs, a.outputs):
-        ref, mag = oracle_entry(e, a.layers, prm, as_np(x, "bf16"), "bf16")
+    for e, x, y, r in zip(a.entries, a.inputs, a.outputs, a.residuals):
+        ref, mag = oracle_entry(e, a.layers, prm, as_np(x, "bf16"), "bf16", None if r is None else as_np(r, "bf16"))
         compare(as_np(y, "bf16"), ref, mag, "bf16", f"{net} {e['op']} {e['layers']}")
         fused += len(e["layers"]) == 2
     assert fused > 0

@@ -103,9 +103,9 @@ def test_executed_plan_entries_match_oracle(net, fmt, path):
     torch.cuda.synchronize()
     prm = onet.params(net, fmt)
     kinds = set()
-    for e, x_dev, y_dev in zip(nw.entries, nw.inputs, nw.outputs):
+    for e, x_dev, y_dev, r_dev in zip(nw.entries, nw.inputs, nw.outputs, nw.residuals):
         x, y = as_np(x_dev, fmt), as_np(y_dev, fmt)
-        ref, mag = oracle_entry(e, nw.layers, prm, x, fmt)
+        ref, mag = oracle_entry(e, nw.layers, prm, x, fmt, None if r_dev is None else as_np(r_dev, fmt))
         compare(y, ref, mag, fmt, f"{net}/{fmt} entry {e['op']} {e['layers']} tile {e.get('tile')}")
         kinds.add(e["op"])
     assert len(kinds) >= 2

@@ -243,3 +243,42 @@ def test_pwpw_int8_intermediate_is_requantised():
             acc = sum(t[c] * int(w2[c, o]) for c in range(3))
             r = (acc * (1 << 30) + (1 << 32)) >> 33
             assert got[n, yy, xx, o] == min(max(r, -128), 127)
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) rank 4 epilogues
+def test_silu_gelu_match_torch_and_closed_forms():
+    """SiLU / GELU of the oracle epilogue vs torch's own F.silu / F.gelu (exact erf form) in fp64,
+    plus closed-form special values and GELU's odd-part identity gelu(v) - gelu(-v) = v."""
+    v = np.concatenate([np.linspace(-12, 12, 2401), [-800.0, -40.0, 0.0, 40.0, 800.0]])
+    tv = torch.from_numpy(v)
+    silu = conv.act_float(v, conv.ACT_SILU)
+    gelu = conv.act_float(v, conv.ACT_GELU)
+    np.testing.assert_allclose(silu, F.silu(tv).numpy(), rtol=1e-15, atol=1e-300)
+    np.testing.assert_allclose(gelu, F.gelu(tv).numpy(), rtol=1e-12, atol=1e-15)  # erf tails differ by ulps
+    assert conv.act_float(np.array([0.0]), conv.ACT_SILU)[0] == 0.0
+    assert conv.act_float(np.array([0.0]), conv.ACT_GELU)[0] == 0.0
+    assert conv.act_float(np.array([40.0]), conv.ACT_SILU)[0] == 40.0 / (1.0 + np.exp(-40.0))
+    assert abs(conv.act_float(np.array([1.0]), conv.ACT_SILU)[0] - 1.0 / (1.0 + np.e ** -1.0)) < 1e-16
+    # sigmoid(0) = 1/2 => silu'(0) = 1/2 ; Phi(1) = 0.8413447460685429 (normal table)
+    assert abs(conv.act_float(np.array([1.0]), conv.ACT_GELU)[0] - 0.8413447460685429) < 1e-15
+    np.testing.assert_allclose(conv.act_float(v, conv.ACT_GELU) - conv.act_float(-v, conv.ACT_GELU), v, atol=1e-12)
+    assert conv.act_float(np.array([-800.0]), conv.ACT_SILU)[0] == 0.0  # -800 * e^-800 underflows
+
+
+def test_residual_add_is_after_activation():
+    """y = round(act(acc*s + b) + r): with act = RELU6 and fp64 the result is exactly the
+    activation output plus r (the shortcut is not clipped), and a zero residual changes nothing."""
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (2, 5, 4, 8))
+    w = rng.uniform(-1, 1, (8, 6))
+    r = rng.uniform(-10, 10, (2, 5, 4, 6))
+    p = {"act": conv.ACT_RELU6, "scale": rng.uniform(0.5, 4, 6), "bias": rng.uniform(-2, 2, 6)}
+    base = conv.pw(x, w, p, "f64")
+    withr = conv.pw(x, w, dict(p, residual=r), "f64")
+    np.testing.assert_array_equal(withr, base + r)
+    assert withr.max() > 6.0 or withr.min() < 0.0  # the sum is outside the RELU6 range: not clipped
+    np.testing.assert_array_equal(conv.pw(x, w, dict(p, residual=np.zeros_like(r)), "f64"), base)
+    # bf16 rounding happens once, after the add
+    bf = conv.pw(x, w, dict(p, residual=r), "bf16")
+    ref = torch.from_numpy(base + r).to(torch.bfloat16).to(torch.float64).numpy()
+    np.testing.assert_array_equal(bf, ref)

@@ -116,7 +116,7 @@ def test_plan_rejects_bad_models(fcm):
 
 
 def test_mobilenet_v2_fuses_every_block_and_saves_bytes(fcm):
-    p = fcm.plan(model_json("mobilenet_v2", "bf16", 256))
+    p = fcm.plan(model_json("mobilenet_v2", "bf16", 256, shortcuts=False))
     assert p["totals"]["fused_pairs"] == 17
     # compulsory bytes: 6605.1 MB LBL -> 2774.1 MB fused
     assert p["totals"]["lbl_dram_bytes"] == 6605130944
