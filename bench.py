@@ -226,37 +226,43 @@ def cpu_baseline(net, dtype, seconds=15.0):
 
 def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5, energy_gpu=None):
     """cuDNN's unfused DW + PW (PyTorch F.conv2d, channels_last, cudnn.benchmark) on the same layers
-    and synthetic weights: BN scale folded into the weights, bias in the conv, activation as an
-    in-place clamp. Captured in a CUDA graph; device time per step via CUDA events."""
+    and synthetic weights: BN scale folded into the weights, bias in the conv, activation in place
+    (clamp / SiLU / GELU), the identity shortcuts as an add after the block's projection, stage /
+    pooled maps fed like the FCM stack. Captured in a CUDA graph; device time per step via CUDA events."""
     import numpy as np
     import torch.nn.functional as F
-    from synth.networks import NETWORKS, layer_ids, network_params
+    from synth.networks import NETWORKS, block_source, layer_ids, network_params
     tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[dtype]
     torch.backends.cudnn.benchmark = True
     prm = network_params(0x5EED, net, dtype)
+    blocks = NETWORKS[net]()
     layers = []
-    for lid, _, l in layer_ids(NETWORKS[net]()):
+    for lid, bi, l in layer_ids(blocks):
         p = prm[lid]
         sc = torch.as_tensor(np.asarray(p["scale"]), dtype=torch.float64)
         if l["kind"] == "dw":
             w = torch.as_tensor(np.asarray(p["w"]), dtype=torch.float64).permute(2, 0, 1)[:, None] * sc[:, None, None, None]
-            layers.append(("dw", w.to(tdt).to(dev).contiguous(memory_format=torch.channels_last),
-                           torch.as_tensor(np.asarray(p["bias"])).to(tdt).to(dev), l))
         else:
             w = (torch.as_tensor(np.asarray(p["w"]), dtype=torch.float64).t() * sc[:, None])[:, :, None, None]
-            layers.append(("pw", w.to(tdt).to(dev).contiguous(memory_format=torch.channels_last),
-                           torch.as_tensor(np.asarray(p["bias"])).to(tdt).to(dev), l))
-    l0 = layers[0][3]
-    c0 = l0["c"] if l0["kind"] == "dw" else l0["c_in"]
-    x = torch.randn(batch, c0, l0["h"], l0["w"], device=dev, dtype=tdt).contiguous(memory_format=torch.channels_last)
+        layers.append((l["kind"], w.to(tdt).to(dev).contiguous(memory_format=torch.channels_last),
+                       torch.as_tensor(np.asarray(p["bias"])).to(tdt).to(dev), l, lid, bi))
+    maps = {}
+
+    def stage_map(bi, l):
+        cin = l["c"] if l["kind"] == "dw" else l["c_in"]
+        key = (l["h"], l["w"], cin)
+        if key not in maps:
+            maps[key] = torch.randn(batch, cin, l["h"], l["w"], device=dev, dtype=tdt).contiguous(
+                memory_format=torch.channels_last)
+        return maps[key]
 
     def run():
-        y = x
-        for kind, w, b, l in layers:
-            cin = l["c"] if kind == "dw" else l["c_in"]
-            if tuple(y.shape[1:]) != (cin, l["h"], l["w"]):  # a stage token map / pooled map input
-                y = torch.zeros(batch, cin, l["h"], l["w"], device=dev, dtype=tdt).contiguous(
-                    memory_format=torch.channels_last)
+        y = None
+        inputs = {}
+        for kind, w, b, l, lid, bi in layers:
+            if y is None or (lid.endswith(".0") and block_source(net, blocks, bi)[0] == "stage"):
+                y = stage_map(bi, l)
+            inputs[lid] = y
             if kind == "dw":
                 y = F.conv2d(y, w, b, stride=l["stride"], padding=l["k"] // 2, groups=l["c"])
             else:
@@ -265,9 +271,13 @@ def cudnn_stack(net, dtype, batch, dev, steps=20, warmup=5, energy_gpu=None):
                 y.clamp_(0, 6)
             elif l["act"] == 1:
                 y.relu_()
+            elif l["act"] == 3:
+                y = F.silu(y, inplace=True)
+            elif l["act"] == 4:
+                y = F.gelu(y)
+            if "residual_from" in l:
+                y.add_(inputs[l["residual_from"]])
         return y
-    if net == "cvt13":
-        return None
     for _ in range(3):
         run()
     torch.cuda.synchronize()
