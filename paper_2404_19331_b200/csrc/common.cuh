@@ -622,18 +622,68 @@ __device__ __forceinline__ void dw3_cols_h(uint32_t src, int row_bytes, const ui
   }
 }
 
-// Segment lengths of the column-pair DW items (rows per item) and their dispatch.
-template <class F>
-__device__ __forceinline__ void with_seg(int seg, F&& f) {
-  switch (seg) {
-    case 14: f(std::integral_constant<int, 14>()); break;
-    case 8: f(std::integral_constant<int, 8>()); break;
-    case 7: f(std::integral_constant<int, 7>()); break;
-    case 4: f(std::integral_constant<int, 4>()); break;
-    case 2: f(std::integral_constant<int, 2>()); break;
-    default: f(std::integral_constant<int, 1>()); break;
+// Rolled form of dw3_cols_h for a RUNTIME number of output rows: output row r is computed whole
+// in iteration r from a 3-row window of staged input words (S = 1: rows r..r+2, one new row per
+// iteration, window period 3; S = 2: rows 2r..2r+2, two new rows per iteration, the even row
+// shared with the next output row, period 2; measured: a 4-buffer variant loading one row ahead
+// was 3 % slower). The loop body is unrolled by the window period so
+// the window rotates through static registers. Same taps in the same (i, j) order per output as
+// dw3_cols_h (bit-identical results). Code size: one period (~3 x 50 instructions) instead of a
+// fully unrolled segment (~750 for 14 rows) -- the SM instruction cache is shared with the other
+// warp roles of the fused kernels and a fully unrolled segment per SEG x activation variant made
+// the DW warps instruction-fetch bound (ncu: 40 % no_instruction stalls).
+template <int DT, int S, int NC, int COLB, class Sink>
+__device__ __forceinline__ void dw3_cols_roll(uint32_t src, int row_bytes, int nrows, const uint32_t (&W)[9],
+                                              Sink&& sink) {
+  constexpr int NCW = (NC - 1) * S + 3;
+  auto load = [&](uint32_t (&dst)[NCW], int row) {
+    const uint32_t rp = src + row * row_bytes;
+#pragma unroll
+    for (int j = 0; j < NCW; ++j) dst[j] = lds32(rp + j * COLB);
+  };
+  auto out_row = [&](int r, const uint32_t (&x0)[NCW], const uint32_t (&x1)[NCW], const uint32_t (&x2)[NCW]) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a, b, x0[c * S + j], W[j]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a, b, x1[c * S + j], W[3 + j]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a, b, x2[c * S + j], W[6 + j]);
+      sink(r, c, a, b);
+    }
+  };
+  if constexpr (S == 1) {
+    uint32_t B0[NCW], B1[NCW], B2[NCW];
+    load(B0, 0);
+    load(B1, 1);
+    for (int r = 0; r < nrows; r += 3) {
+      load(B2, r + 2);
+      out_row(r, B0, B1, B2);
+      if (r + 1 >= nrows) break;
+      load(B0, r + 3);
+      out_row(r + 1, B1, B2, B0);
+      if (r + 2 >= nrows) break;
+      load(B1, r + 4);
+      out_row(r + 2, B2, B0, B1);
+    }
+  } else {
+    uint32_t E0[NCW], E1[NCW], O[NCW];
+    load(E0, 0);
+    for (int r = 0; r < nrows; r += 2) {
+      load(O, 2 * r + 1);
+      load(E1, 2 * r + 2);
+      out_row(r, E0, O, E1);
+      if (r + 1 >= nrows) break;
+      load(O, 2 * r + 3);
+      load(E0, 2 * r + 4);
+      out_row(r + 1, E1, O, E0);
+    }
   }
 }
+
+// Activation dispatch: one instantiation per activation (the runtime value picks it once).
 template <class F>
 __device__ __forceinline__ void with_act(int act, F&& f) {
   if (act == FCM_ACT_RELU6) f(std::integral_constant<int, 2>());

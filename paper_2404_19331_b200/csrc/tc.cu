@@ -45,8 +45,7 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return d;
 }
 
-// Epilogue of 16 accumulator columns [n_base, n_base+16) of one row -> packed storage words.
-// Constants come from smem as 128-bit broadcast loads (n_base is a multiple of 16).
+// A packed bf16x2 / f16x2 word -> its two fp32 values (lo, hi).
 template <int DT>
 __device__ __forceinline__ float2 word2f(uint32_t w) {
   if constexpr (DT == FCM_BF16) return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
@@ -54,11 +53,15 @@ __device__ __forceinline__ float2 word2f(uint32_t w) {
 }
 
 // Epilogue of 16 accumulator columns [n_base, n_base+16) of one row -> packed storage words.
-// Constants come from smem as 128-bit broadcast loads (n_base is a multiple of 16). rw (bf16 / f16
-// only): the 8 packed words of the residual (shortcut) for these 16 columns, or nullptr.
-template <int DT>
+// Constants come from smem as 128-bit broadcast loads (n_base is a multiple of 16).
+// RES (bf16 / f16): ra / rb = the 8 packed words of the residual (shortcut) for these 16 columns,
+// added after the activation. The activation variants are dispatched once per
+// call, so a kernel only fetches the code it runs (the DWPW epilogue shares the SM's instruction
+// cache with the DW stage's hot loop; measured: a per-element activation switch with erf inlined 16x
+// cost the DW warps 2x in instruction-fetch stalls).
+template <int DT, bool RES = false>
 __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
-                                      uint32_t (&out)[8], const uint32_t* rw = nullptr) {
+                                      uint32_t (&out)[8], uint4 ra = uint4{}, uint4 rb = uint4{}) {
   if constexpr (DT == FCM_S8) {
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -76,31 +79,6 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
       out[w] = word;
     }
   } else {
-    if (rw || e.act > FCM_ACT_RELU6) {
-      // SiLU / GELU and / or the residual: 4 columns at a time (registers);
-      // the activation is dispatched once per call, so only one variant's code is fetched (the
-      // DWPW epilogue shares the SM's instruction cache with the DW stage's hot loop)
-      with_act(e.act, [&](auto actc) {
-        constexpr int ACT = decltype(actc)::value;
-        // GELU's erf is ~30 instructions: keep its loop rolled (instruction-cache footprint)
-#pragma unroll(ACT == FCM_ACT_GELU ? 1 : 4)
-        for (int q = 0; q < 4; ++q) {
-          const uint4 a = lds128(cs.base + 4 * (n_base + 4 * q));
-          const uint4 b = lds128(cs.base + 4 * (cs.ncap + n_base + 4 * q));
-          float v0 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q]), __uint_as_float(a.x), __uint_as_float(b.x)));
-          float v1 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q + 1]), __uint_as_float(a.y), __uint_as_float(b.y)));
-          float v2 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q + 2]), __uint_as_float(a.z), __uint_as_float(b.z)));
-          float v3 = act_t<ACT>(fmaf(__uint_as_float(r[4 * q + 3]), __uint_as_float(a.w), __uint_as_float(b.w)));
-          if (rw) {
-            const float2 s0 = word2f<DT>(rw[2 * q]), s1 = word2f<DT>(rw[2 * q + 1]);
-            v0 += s0.x; v1 += s0.y; v2 += s1.x; v3 += s1.y;
-          }
-          out[2 * q] = pack2<DT, false>(v0, v1);
-          out[2 * q + 1] = pack2<DT, false>(v2, v3);
-        }
-      });
-      return;
-    }
     float sc[16], bi[16];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -111,8 +89,38 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
       bi[4 * q] = __uint_as_float(b.x); bi[4 * q + 1] = __uint_as_float(b.y);
       bi[4 * q + 2] = __uint_as_float(b.z); bi[4 * q + 3] = __uint_as_float(b.w);
     }
+    if (e.act > FCM_ACT_RELU6) {
+      // SiLU / GELU (+ residual): the activation dispatched once per call (one variant's code is
+      // fetched; a rolled loop would move r / out to local memory)
+      with_act(e.act, [&](auto actc) {
+        constexpr int ACT = decltype(actc)::value;
+        const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          float v0 = act_t<ACT>(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]));
+          float v1 = act_t<ACT>(fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]));
+          if constexpr (RES) {
+            const float2 s = word2f<DT>(rw[w]);
+            v0 += s.x;
+            v1 += s.y;
+          }
+          out[w] = pack2<DT, false>(v0, v1);
+        }
+      });
+      return;
+    }
     const float hi_c = act_hi(e.act);
-    if (e.act == FCM_ACT_NONE) {
+    if constexpr (RES) {
+      const float lo_c = act_lo(e.act);
+      const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const float2 s = word2f<DT>(rw[w]);
+        out[w] = pack2<DT, false>(
+            fminf(fmaxf(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]), lo_c), hi_c) + s.x,
+            fminf(fmaxf(fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]), lo_c), hi_c) + s.y);
+      }
+    } else if (e.act == FCM_ACT_NONE) {
 #pragma unroll
       for (int w = 0; w < 8; ++w)
         out[w] = pack2<DT, false>(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]),
@@ -123,6 +131,19 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
         out[w] = pack2<DT, true>(fminf(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]), hi_c),
                                  fminf(fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]), hi_c));
     }
+  }
+}
+
+// One 16-column epilogue step of a float (bf16 / f16) output with the runtime activation / residual
+// choice; r points at 16 consecutive accumulator words.
+template <int DT>
+__device__ __forceinline__ void epi16_any(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
+                                          uint32_t (&out)[8], bool res, uint4 ra, uint4 rb) {
+  if constexpr (DT == FCM_S8) {
+    epi16<DT>(r, cs, e, n_base, out);
+  } else {
+    if (res) epi16<DT, true>(r, cs, e, n_base, out, ra, rb);
+    else epi16<DT>(r, cs, e, n_base, out);
   }
 }
 
@@ -179,7 +200,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tacc, int BN, int n0, int
       tmem_ld16(tacc + ((uint32_t)(q * 32) << 16) + c0, r);
       tmem_ld_wait();
       uint32_t o[8];
-      epi16<DT>(r, cs, e, n0 + c0, o);
+      epi16_any<DT>(r, cs, e, n0 + c0, o, false, uint4{}, uint4{});
 #pragma unroll
       for (int v = 0; v < ES; ++v)
         sts128(smem_u32(buf) + sw128_vec(m, j * ES + v), o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
@@ -235,7 +256,7 @@ __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0
           tmem_ld16(tacc + ((uint32_t)(q * 32) << 16) + c0 + 16 * hh, r);
           tmem_ld_wait();
           uint32_t o[8];
-          epi16<DT>(r, cs, e, col, o, hasres ? reinterpret_cast<const uint32_t*>(rw) : nullptr);
+          epi16_any<DT>(r, cs, e, col, o, hasres, rw[0], rw[1]);
           const int vi0 = (c32 + 16 * hh) * ES / 16;
 #pragma unroll
           for (int v = 0; v < ES; ++v)
@@ -684,8 +705,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           // item reads only staged rows and stores unpredicated (slots past the item count excepted)
           const int seg_sel = (dv.seg_sel >> (8 * gi)) & 0xFF;
           const FDiv fnsg = gi == 0 ? dv.nsg[0] : (gi == 1 ? dv.nsg[1] : dv.nsg[2]);  // no dynamic param index (-> stack)
-          with_seg(seg_sel, [&](auto segc) {
-            constexpr int SEG = decltype(segc)::value;
+          {
+            const int SEG = seg_sel;  // rows per item (runtime: the rolled core has one code path)
             with_act(ed.act, [&](auto actc) {
               constexpr int ACT = decltype(actc)::value;
               const int nsg = (th + SEG - 1) / SEG;
@@ -702,13 +723,13 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
                 const uint32_t src = st + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * 32 + wd) * 4;
                 const bool p1 = live && x0 + 1 < tw;
                 const uint32_t a0 = abase + lane_off + (uint32_t)((b * th + y0) * tw + x0) * 16;
-                dw3_cols_h<DT, S, SEG, 2, 128>(src, tw_in * 128, W9, [&](int r, int c, float lo, float hi) {
+                dw3_cols_roll<DT, S, 2, 128>(src, tw_in * 128, SEG, W9, [&](int r, int c, float lo, float hi) {
                   const uint32_t v = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
                   if (c == 0 ? live : p1) sts32(a0 + r * rstep + c * 16, v);
                 });
               }
             });
-          });
+          }
         } else {
          bool done = false;
          if constexpr (DT == FCM_S8 && K == 3) {
@@ -865,23 +886,16 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             if (c0 + 32 < valid) res32_load(ep.residual, poh, c0 + 32, valid, ok, rnext);
             else if (h + 1 < MB) res32_load(ep.residual, po1, 0, valid, pok1, rnext);
           }
-          uint32_t r[32];
-          tmem_ld32(tq + c0, r);
-          tmem_ld_wait();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int cb = c0 + 16 * hh;  // 16 columns = 2 x 8-column (16 B bf16 / 8 B int8) pieces
             if (cb >= valid) break;
+            uint32_t r[16];
+            tmem_ld16(tq + cb, r);
+            tmem_ld_wait();
             uint32_t o[8];
-            if constexpr (ES == 2) {
-              if (hasres) {  // the shortcut input at the same NHWC position
-                epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o, reinterpret_cast<const uint32_t*>(&rcur.v[2 * hh]));
-              } else {
-                epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o);
-              }
-            } else {
-              epi16<DT>(&r[16 * hh], cs, ep, ns * BN + cb, o);
-            }
+            // (the residual: the shortcut input at the same NHWC position)
+            epi16_any<DT>(r, cs, ep, ns * BN + cb, o, hasres, rcur.v[2 * hh], rcur.v[2 * hh + 1]);
             if (ok) {
               if constexpr (ES == 2) {
                 stg128(dst + cb * 2, o[0], o[1], o[2], o[3]);
@@ -1115,7 +1129,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
             for (int hh = 0; hh < 2; ++hh) {
               const int c0 = h * CPW + 32 * u + 16 * hh;
               uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              if (inside) epi16<DT>(&rg[16 * hh], cs, ep, sl * TD + c0, o);
+              if (inside) epi16_any<DT>(&rg[16 * hh], cs, ep, sl * TD + c0, o, false, uint4{}, uint4{});
               const uint32_t dst = smem_u32(tb) + r * PITCH + c0 * ES;
 #pragma unroll
               for (int v = 0; v < ES; ++v) sts128(dst + 16 * v, o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
@@ -1161,8 +1175,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
         const int hp = (tw + 1) >> 1;
         group_wait(Tfull + tbi, (local / depth) & 1, dw == 0, 3, kPwdwNDW * 32);
         if (dw == 0 && lane == 0) stamp(local, 6);
-        with_seg(dv.seg, [&](auto segc) {
-          constexpr int SEG = decltype(segc)::value;
+        {
+          const int SEG = dv.seg;  // rows per item (runtime, rolled core)
           with_act(ed.act, [&](auto actc) {
             constexpr int ACT = decltype(actc)::value;
             const int nsg = (th + SEG - 1) / SEG;
@@ -1181,13 +1195,13 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
               const bool c0ok = cval, c1ok = cval && (x0 + 1 < tw) && (xo + 1 < Wo);
               uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
               const size_t rstride = (size_t)Wo * Cmid / V, cstride = (size_t)Cmid / V;
-              dw3_cols_h<DT, S, SEG, 2, PITCH>(src, tw_in * PITCH, W9, [&](int r, int cc, float lo, float hi) {
+              dw3_cols_roll<DT, S, 2, PITCH>(src, tw_in * PITCH, SEG, W9, [&](int r, int cc, float lo, float hi) {
                 if (r < nvalid && (cc == 0 ? c0ok : c1ok))
                   dst[r * rstride + cc * cstride] = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
               });
             }
           });
-        });
+        }
       } else {
         DwW<DT, K> Wd;
         load_dw_weights_smem<DT, K>(Wd, wsm, nslice * 32, sl * 32 + lane);
@@ -1361,8 +1375,7 @@ static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
   for (int gi = 0; gi < 3; ++gi) {
     const int slots = 1 << gi;
     int best = 1, bcost = 1 << 30;
-    for (int seg : {14, 8, 7, 4, 2, 1}) {
-      if (seg > g.th) continue;  // a segment never leaves the tile (ragged segments shift up)
+    for (int seg = std::min(g.th, 32); seg >= 1; --seg) {  // any length (rolled core); ragged ones shift up
       const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
       const int rounds = ((nit + slots - 1) / slots + ndw - 1) / ndw;
       const int cost = rounds * ((seg - 1) * S + K + 2);
@@ -1427,12 +1440,17 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   int grid = std::min(total, device_props().sms);
   int BS = 2;
   static const int xs_cap = [] { const char* e = getenv("FCM_XS_MAX"); return e ? atoi(e) : 6; }();  // dev override
-  int XS = std::min(xs_cap, (device_props().smem_optin - fixed - BS * BN * 128) / xstride);
+#ifdef FCM_TRACE_STAMPS
+  const int smem_cap = device_props().smem_optin - 64 * 12 * 8;  // the trace build's static stamp buffer
+#else
+  const int smem_cap = device_props().smem_optin;
+#endif
+  int XS = std::min(xs_cap, (smem_cap - fixed - BS * BN * 128) / xstride);
   if (XS < 2) return set_error(FCM_E_INFEASIBLE, "dwpw: tile too large for 2 X stages");
   // resident weights: grid a multiple of nsplit fixes each CTA's C_out slice; keep all nk chunks
   // when that costs at most one X stage (and leaves >= 2)
   const int resgrid = (grid / nsplit) * nsplit;
-  const int xs_res = std::min(xs_cap, (device_props().smem_optin - fixed - nk * BN * 128) / xstride);
+  const int xs_res = std::min(xs_cap, (smem_cap - fixed - nk * BN * 128) / xstride);
   const bool resB = nk <= 16 && resgrid > 0 && resgrid >= grid * 15 / 16 && xs_res >= 2 && xs_res >= XS - 1;
   if (resB) {
     grid = resgrid;
@@ -1480,8 +1498,7 @@ template <int DT, int K, int S>
 static PwdwDivs pwdw_divs(const Geo& g, int nslice, int tiles_x, int tiles_y) {
   const int hp = (g.tw + 1) / 2;
   int best = 1, bcost = 1 << 30;
-  for (int seg : {14, 8, 7, 4, 2, 1}) {
-    if (seg > g.th) continue;  // segments never leave the tile (ragged ones shift up)
+  for (int seg = std::min(g.th, 32); seg >= 1; --seg) {  // any length (rolled core); ragged ones shift up
     const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
     const int rounds = (nit + kPwdwNDW - 1) / kPwdwNDW;
     const int cost = rounds * ((seg - 1) * S + K + 2);
@@ -1745,7 +1762,7 @@ __global__ void __launch_bounds__(608, 1)
           uint32_t r[16];
           tmem_ld16(tacc1 + ((uint32_t)(q * 32) << 16) + c0, r);
           tmem_ld_wait();
-          epi16<DT>(r, cs1, ep1, c0, o);
+          epi16_any<DT>(r, cs1, ep1, c0, o, false, uint4{}, uint4{});
         }
         const int kc = c0 / KC, vi0 = (c0 % KC) * ES / 16;
 #pragma unroll

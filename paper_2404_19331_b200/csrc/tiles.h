@@ -66,8 +66,7 @@ inline long dwpw_pair_cost(const Geo& g, int nb, int th, int tw, int sms = 148) 
   const long tiles = (long)((g.N + nb - 1) / nb) * ((g.Ho + th - 1) / th) * ((g.Wo + tw - 1) / tw);
   const int hp = (tw + 1) / 2;
   long best = -1;
-  for (int seg : {14, 8, 7, 4, 2, 1}) {
-    if (seg > th) continue;
+  for (int seg = std::min(th, 32); seg >= 1; --seg) {
     const int items = nb * hp * ((th + seg - 1) / seg);
     const long t = (long)((items + 7) / 8) * ((seg - 1) * g.s + 3 + 2);
     if (best < 0 || t < best) best = t;
