@@ -76,6 +76,38 @@ def dwpw_tile_alternatives(tile, ho, wo, k, s, cout, dtype, limit=10):
     return [uniq[0]] + rest[:limit - 1]
 
 
+def pwdw_tile_alternatives(tile, ho, wo, k, s, dtype, limit=10):
+    """PWDW_R output tiles besides the planner's: the PW runs over the tile's halo, whose rows are
+    the MMA rows (<= 512 for bf16/f16 -- 4 row blocks x 64 T columns x 2 TMEM buffers -- else 256);
+    larger tiles recompute less halo, smaller ones give more tiles (measured, not modelled)."""
+    rmax = 512 if dtype in ("bf16", "f16") else 256
+    out = [dict(tile)]
+    sizes = [4, 7, 8, 10, 12, 14, 16, 28]
+    for th in sizes:
+        for tw in sizes:
+            th, tw = min(th, ho), min(tw, wo)
+            th_in, tw_in = (th - 1) * s + k, (tw - 1) * s + k
+            if th_in * tw_in > rmax or th * tw < 16:
+                continue
+            out.append({"tile_n": 1, "tile_h": th, "tile_w": tw, "n_split": tile.get("n_split", 1)})
+    if k * k <= rmax:
+        hw_in = ((ho - 1) * s + k) * ((wo - 1) * s + k)
+        for nb in range(2, rmax // hw_in + 1):
+            out.append({"tile_n": nb, "tile_h": ho, "tile_w": wo, "n_split": tile.get("n_split", 1)})
+    seen, uniq = set(), []
+    for t in out:
+        key = (t["tile_n"], t["tile_h"], t["tile_w"])
+        if key not in seen:
+            seen.add(key)
+            uniq.append(t)
+    # largest outputs per halo row first (least recompute), then the rest
+    def eff(t):
+        r = t["tile_n"] * ((t["tile_h"] - 1) * s + k) * ((t["tile_w"] - 1) * s + k)
+        return -t["tile_n"] * t["tile_h"] * t["tile_w"] / r
+    rest = sorted(uniq[1:], key=eff)
+    return [uniq[0]] + rest[:limit - 1]
+
+
 def dw_tile_alternatives(tile, ho, wo, k, s, c, dtype):
     """LBL DW output tiles besides the planner's default: small tiles give more CTAs (latency
     hiding on small maps), large ones less halo; the measurement picks."""
@@ -120,7 +152,7 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
     probe = Network(net, dtype, batch, {"entries": []}, device=device)
     all_entries += pwpw_candidates(model_json(net, dtype, batch), probe, dtype, batch)
     order = probe.order
-    meas = {}
+    meas, report = {}, []
     for c in all_entries:
         lids = c["layers"]
         l0 = probe.layers[lids[0]]
@@ -135,6 +167,12 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
             ho = (d["h"] + 2 * (kk // 2) - kk) // ss + 1
             wo = (d["w"] + 2 * (kk // 2) - kk) // ss + 1
             tiles = dwpw_tile_alternatives(c["tile"], ho, wo, kk, ss, probe.layers[lids[1]]["c_out"], dtype)
+        elif tile_search and c["op"] == "pwdw_r" and c.get("tile") and dtype in ("bf16", "f16", "s8"):
+            d = probe.layers[lids[1]]
+            kk, ss = d["k"], d["stride"]
+            ho = (d["h"] + 2 * (kk // 2) - kk) // ss + 1
+            wo = (d["w"] + 2 * (kk // 2) - kk) // ss + 1
+            tiles = pwdw_tile_alternatives(c["tile"], ho, wo, kk, ss, dtype)
         elif tile_search and c["op"] == "dw" and c.get("tile") and c["tile"].get("tile_w", 0) > 1:
             d = probe.layers[lids[0]]
             kk, ss = d["k"], d["stride"]
@@ -154,6 +192,7 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
             if best is None or us < best[0]:
                 best = (us, t)
         if best is not None:
+            report.append({"op": c["op"], "layers": lids, "tile": best[1], "us": round(best[0], 2)})
             meas[tuple(lids)] = best[0]
             if best[1] is not None:
                 c["tile"] = best[1]
@@ -173,6 +212,7 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
     out["totals"] = dict(plan["totals"], measured_us=total, dram_bytes=sum(e["dram_bytes"] for e in entries),
                          fused_pairs=sum(1 for e in entries if len(e["layers"]) == 2))
     out.pop("candidates", None)
+    out["measured_candidates"] = report
     return out
 
 

@@ -632,6 +632,9 @@ __device__ __forceinline__ void dw3_cols_h(uint32_t src, int row_bytes, const ui
 // fully unrolled segment (~750 for 14 rows) -- the SM instruction cache is shared with the other
 // warp roles of the fused kernels and a fully unrolled segment per SEG x activation variant made
 // the DW warps instruction-fetch bound (ncu: 40 % no_instruction stalls).
+#ifndef FCM_DW_SPLIT  // measured: no gain in DWPW (b8 30.3 -> 31.2 us), kept as a development switch
+#define FCM_DW_SPLIT 0
+#endif
 template <int DT, int S, int NC, int COLB, class Sink>
 __device__ __forceinline__ void dw3_cols_roll(uint32_t src, int row_bytes, int nrows, const uint32_t (&W)[9],
                                               Sink&& sink) {
@@ -644,6 +647,23 @@ __device__ __forceinline__ void dw3_cols_roll(uint32_t src, int row_bytes, int n
   auto out_row = [&](int r, const uint32_t (&x0)[NCW], const uint32_t (&x1)[NCW], const uint32_t (&x2)[NCW]) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
+#if FCM_DW_SPLIT
+      // one partial sum per filter row (three 3-deep FHFMA chains instead of one 9-deep chain per
+      // output half: the DW warps are latency-bound at two warps per SM sub-partition), summed
+      // with two packed adds: (p0 + p1) + p2
+      float a[3] = {0.f, 0.f, 0.f}, b[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a[0], b[0], x0[c * S + j], W[j]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a[1], b[1], x1[c * S + j], W[3 + j]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a[2], b[2], x2[c * S + j], W[6 + j]);
+      const uint64_t one2 = 0x3F8000003F800000ull;
+      const uint64_t s = f2_fma(f2_pack(a[2], b[2]), one2, f2_fma(f2_pack(a[0], b[0]), one2, f2_pack(a[1], b[1])));
+      float lo, hi;
+      f2_unpack(s, lo, hi);
+      sink(r, c, lo, hi);
+#else
       float a = 0.f, b = 0.f;
 #pragma unroll
       for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a, b, x0[c * S + j], W[j]);
@@ -652,6 +672,7 @@ __device__ __forceinline__ void dw3_cols_roll(uint32_t src, int row_bytes, int n
 #pragma unroll
       for (int j = 0; j < 3; ++j) hfma2_acc<DT>(a, b, x2[c * S + j], W[6 + j]);
       sink(r, c, a, b);
+#endif
     }
   };
   if constexpr (S == 1) {

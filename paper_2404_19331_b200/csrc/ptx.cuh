@@ -202,6 +202,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   return d;
 }
 
+// K-major operand with a 32 / 64 / 128-byte swizzle (rows of xb bytes, as TMA writes a box whose
+// inner extent is xb bytes with the matching CU_TENSOR_MAP_SWIZZLE_*): 8-row atoms, SBO = 8 * xb;
+// layout type 6 (32B), 4 (64B), 2 (128B)
+__device__ __forceinline__ uint64_t smem_desc_swz(uint32_t saddr, int xb) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>((8 * xb) >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(xb == 128 ? 2 : (xb == 64 ? 4 : 6)) << 61;
+  return d;
+}
+
 // Instruction descriptor (kind::f16 / kind::tf32 / kind::i8), both operands K-major.
 //   c_fmt: 1 = F32, 2 = S32;  ab_fmt: f16 0, bf16 1, tf32 2; i8: 1 = signed
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t c_fmt, uint32_t ab_fmt, uint32_t M, uint32_t N) {

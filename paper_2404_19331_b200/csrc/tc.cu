@@ -447,6 +447,13 @@ __global__ void __launch_bounds__(576, 1)
 #ifndef FCM_DWPW_RELAY
 #define FCM_DWPW_RELAY 1
 #endif
+// output columns per DW item of the bf16/f16 3x3 core (a lane owns one channel word of NC adjacent
+// columns): 4 gives each warp 8 independent accumulation chains per row (2 -> 4 was 2-3x faster on
+// the 14 x 14 tiles, whose few items left one latency-bound warp per phase on the critical path)
+#ifndef FCM_DWPW_NC
+#define FCM_DWPW_NC 4
+#endif
+constexpr int kDwpwNC = FCM_DWPW_NC;
 template <int DT, int K> constexpr int dwpw_ndw() { return FCM_DWPW_NDW; }
 constexpr int kDwpwNA = 2;  // default A-operand (commBuffer) ring depth
 struct DwDivs {
@@ -692,17 +699,18 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             kc_w = kc;
           }
           const uint32_t lane_off = (wd >> 2) * albo + (wd & 3) * 4;
-          const int hp = (tw + 1) >> 1;   // column pairs per image row
+          constexpr int NC = kDwpwNC;
+          const int hp = (tw + NC - 1) / NC;   // column groups per image row
           const int ncp = nb * hp;
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 10);
           if (dw == 0 && lane == 0) cstamp(phase, 2);
           go();
           if (dw == 0 && lane == 0) cstamp(phase, 3);
           if (dw == 0 && lane == 0 && kc == 0) stamp(local, 11);
-          // item = (column pair, segment of SEG rows); SEG (<= th) chosen on the host per lane-group
-          // width. A ragged last segment / odd last column pair is shifted back inside the tile
-          // (y0 = th - SEG, x0 = tw - 2): the overlap is recomputed with identical values, so every
-          // item reads only staged rows and stores unpredicated (slots past the item count excepted)
+          // item = (group of NC columns, segment of SEG rows); SEG (<= th) chosen on the host per
+          // lane-group width. A ragged last segment / column group is shifted back inside the tile
+          // (y0 = th - SEG, x0 = tw - NC): the overlap is recomputed with identical values, so every
+          // item reads only staged rows (columns past a tile narrower than NC are not stored)
           const int seg_sel = (dv.seg_sel >> (8 * gi)) & 0xFF;
           const FDiv fnsg = gi == 0 ? dv.nsg[0] : (gi == 1 ? dv.nsg[1] : dv.nsg[2]);  // no dynamic param index (-> stack)
           {
@@ -718,14 +726,14 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
                 const int iv = live ? item : 0;
                 const int cp = fdiv(iv, fnsg), seg = iv - cp * nsg;
                 const int b = fdiv(cp, dv.hp);
-                const int x0 = max(0, min(2 * (cp - b * hp), tw - 2));
+                const int x0 = max(0, min(NC * (cp - b * hp), tw - NC));
                 const int y0 = min(seg * SEG, th - SEG);
                 const uint32_t src = st + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * 32 + wd) * 4;
-                const bool p1 = live && x0 + 1 < tw;
+                const int ncv = live ? min(NC, tw - x0) : 0;  // columns this lane stores
                 const uint32_t a0 = abase + lane_off + (uint32_t)((b * th + y0) * tw + x0) * 16;
-                dw3_cols_roll<DT, S, 2, 128>(src, tw_in * 128, SEG, W9, [&](int r, int c, float lo, float hi) {
+                dw3_cols_roll<DT, S, NC, 128>(src, tw_in * 128, SEG, W9, [&](int r, int c, float lo, float hi) {
                   const uint32_t v = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
-                  if (c == 0 ? live : p1) sts32(a0 + r * rstep + c * 16, v);
+                  if (c < ncv) sts32(a0 + r * rstep + c * 16, v);
                 });
               }
             });
@@ -943,8 +951,10 @@ template <int DT, int K, int S> constexpr int pwdw_seg() {
 }
 struct PwdwDivs {
   FDiv nslice, tx, ty, tw, nseg;  // tile decode + DW item decode
-  FDiv hp, nsg;                   // pair core: column pairs per image, ceil(th / seg)
-  int seg;                        // pair core segment length (4, 7, 8 or 14)
+  FDiv hp, nsg;                   // pair core: column groups per image, ceil(th / seg)
+  int seg;                        // pair core segment length
+  FDiv thw_in, tw_in;             // T producers: halo row r -> (image, row, column)
+  FDiv rot;                       // slice rotation period (spatial tiles per round of the grid)
 };
 template <int DT, int K> constexpr bool pwdw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
 template <int DT, int K> constexpr int pwdw_wbytes(int nslice) {
@@ -957,7 +967,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
                    const typename Tr<DT>::T* __restrict__ wdw, Epi ep, Epi ed, uint8_t* __restrict__ y, int N, int H,
                    int W, int Cin, int Ho, int Wo, int Cmid, int pt, int pl, int nb, int th, int tw, int tiles_x,
                    int tiles_y, int stages, int depth, uint32_t tmem_cols, int ncap, int resB, PwdwDivs dv,
-                   int dbg, unsigned long long* trace) {
+                   int xb, int dbg, unsigned long long* trace) {
   pdl_launch();
   constexpr int ES = Tr<DT>::ES;
   constexpr int V = Tr<DT>::VEC;
@@ -972,8 +982,10 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   const int th_in = (th - 1) * S + K, tw_in = (tw - 1) * S + K;
   const int R = nb * th_in * tw_in;
   const int MB = (R + 127) / 128;
-  const int xbytes = R * 128;
-  const int astride = MB * 16384;
+  // X halo rows of xb bytes (32 / 64 / 128: a C_in below 64 channels is staged at its own width,
+  // not as 128-byte rows that are mostly out-of-bounds fill)
+  const int xbytes = R * xb;
+  const int astride = MB * 128 * xb;
   const int stage_bytes = astride + (resB ? 0 : TD * 128);
   const int tbytes = ((R * PITCH) + 1023) & ~1023;
   const int nslice = (Cmid + TD - 1) / TD;
@@ -981,8 +993,11 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* tsm = smem + stages * stage_bytes;  // `depth` T buffers
-  uint8_t* bres = tsm + depth * tbytes;        // resB: this CTA's PW weight slice, all nk chunks
-  uint8_t* cst = bres + (resB ? nk * TD * 128 : 0);
+  // resB 1: all PW weight slices x nk chunks resident; 2: only this CTA's slice (grid a multiple of
+  // nslice, no slice rotation: the CTA's slice is fixed)
+  const int nres = resB == 1 ? nslice : 1;
+  uint8_t* bres = tsm + depth * tbytes;
+  uint8_t* cst = bres + (resB ? nk * nres * TD * 128 : 0);
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(ncap));
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(wsm) + pwdw_wbytes<DT, K>(nslice));
@@ -1028,9 +1043,16 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
   auto stamp = [&](int local, int ev) {
     if (trace && blockIdx.x == 0 && local < 64) trace[local * 16 + ev] = clock64();
   };
+  // tile t -> (spatial tile sp, C_mid slice): the slices of one spatial tile are consecutive tiles
+  // (their X halo is one L2 fetch), rotated by sp / (grid / nslice) so that every CTA cycles
+  // through the slices (a partly filled last slice is cheaper; a fixed slice per CTA left the
+  // full-slice CTAs on the critical path)
   auto decode = [&](int t, int& sl, int& nbi, int& tyi, int& txi) {
     int sp = fdiv(t, dv.nslice);
     sl = t - sp * nslice;
+    const int rot = fdiv(sp, dv.rot);
+    sl += rot - fdiv(rot, dv.nslice) * nslice;
+    if (sl >= nslice) sl -= nslice;
     int q = fdiv(sp, dv.tx);
     txi = sp - q * tiles_x;
     nbi = fdiv(q, dv.ty);
@@ -1041,10 +1063,12 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     if (lane == 0) {
       const uint32_t tx = xbytes + (resB ? 0 : TD * 128);
       int it = 0;
-      if (resB) {  // grid is a multiple of nslice: this CTA's C_mid slice is fixed, load its weights once
-        mbar_arrive_expect_tx(bfull, nk * TD * 128);
+      if (resB) {  // resident weight slices: loaded once per CTA
+        mbar_arrive_expect_tx(bfull, nk * nres * TD * 128);
         for (int kc = 0; kc < nk; ++kc)
-          tma_load_2d(bres + kc * TD * 128, &tmb, bfull, kc * KC, (blockIdx.x % nslice) * TD);
+          for (int s2 = 0; s2 < nres; ++s2)
+            tma_load_2d(bres + (kc * nres + s2) * TD * 128, &tmb, bfull, kc * KC,
+                        (resB == 1 ? s2 : blockIdx.x % nslice) * TD);
       }
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int sl, nbi, tyi, txi;
@@ -1071,6 +1095,8 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       if (resB) mbar_wait(bfull, 0);
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const int acc = local % depth;
+        int sl, nbi, tyi, txi;
+        decode(t, sl, nbi, tyi, txi);
         mbar_wait(tempty + acc, ((local / depth) & 1) ^ 1);
         stamp(local, 0);
         tc_fence_after();
@@ -1080,11 +1106,12 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
           if (kc == 0) stamp(local, 1);
           tc_fence_after();
           uint8_t* st = smem + s * stage_bytes;
-          const uint64_t bd = smem_desc_sw128(smem_u32(resB ? bres + kc * TD * 128 : st + astride));
+          const uint64_t bd =
+              smem_desc_sw128(smem_u32(resB ? bres + (kc * nres + (resB == 1 ? sl : 0)) * TD * 128 : st + astride));
           for (int mb = 0; mb < MB; ++mb) {
-            const uint64_t ad = smem_desc_sw128(smem_u32(st + mb * 16384));
+            const uint64_t ad = smem_desc_swz(smem_u32(st + mb * 128 * xb), xb);
             const uint32_t d = tbase + acc * acc_cols + mb * TD;
-            const int ksteps = min(4, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
+            const int ksteps = min(xb / 32, (Cin - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
             for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
           }
           mma_commit(empty + s);
@@ -1113,29 +1140,63 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       }
       named_bar_sync(2, NTP * 32);
       tc_fence_after();
-      for (int mb = 0; mb < MB && !(dbg & 2); ++mb) {
-        const int r = mb * 128 + q * 32 + lane;
-        const int b = r / (th_in * tw_in), rr = r - b * th_in * tw_in;
-        const int yi = tyi * th * S - pt + rr / tw_in, xi = txi * tw * S - pl + rr % tw_in;
-        const int n = nbi * nb + b;
-        const bool inside = (r < R) && (n < N) && (yi >= 0) && (yi < H) && (xi >= 0) && (xi < W);
+      // eps_pw of 16 accumulator columns -> 8 T words: the packed bf16 / f16 fast path (FFMA2 affine,
+      // cvt.rn(.relu) pack, min for RELU6 -- identical to the scalar fma / min / round) for the
+      // clamp activations, the generic epilogue for SiLU / GELU and int8
+      auto produce = [&](auto actc) {
+        constexpr int ACT = decltype(actc)::value;
+        const uint32_t hi_c = (ES == 2 && ACT == FCM_ACT_RELU6) ? bound2<DT>(6.f) : 0u;
+        for (int mb = 0; mb < MB && !(dbg & 2); ++mb) {
+          const int r = mb * 128 + q * 32 + lane;
+          const int b = fdiv(r, dv.thw_in), rr = r - b * th_in * tw_in;
+          const int ry = fdiv(rr, dv.tw_in);
+          const int yi = tyi * th * S - pt + ry, xi = txi * tw * S - pl + (rr - ry * tw_in);
+          const int n = nbi * nb + b;
+          const bool inside = (r < R) && (n < N) && (yi >= 0) && (yi < H) && (xi >= 0) && (xi < W);
 #pragma unroll 1
-        for (int u = 0; u < NU; ++u) {
-          uint32_t rg[32];
-          tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * acc_cols + mb * TD + h * CPW + 32 * u, rg);
-          tmem_ld_wait();  // one round trip per 32 columns
-          if (r < R) {
+          for (int u = 0; u < NU; ++u) {
+            if (sl * TD + h * CPW + 32 * u >= Cmid) break;  // columns past C_mid: never read by the DW
+            uint32_t rg[32];
+            tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * acc_cols + mb * TD + h * CPW + 32 * u, rg);
+            tmem_ld_wait();  // one round trip per 32 columns
+            if (r < R) {
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const int c0 = h * CPW + 32 * u + 16 * hh;
-              uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              if (inside) epi16_any<DT>(&rg[16 * hh], cs, ep, sl * TD + c0, o, false, uint4{}, uint4{});
-              const uint32_t dst = smem_u32(tb) + r * PITCH + c0 * ES;
+              for (int hh = 0; hh < 2; ++hh) {
+                const int c0 = h * CPW + 32 * u + 16 * hh;
+                uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                if (inside) {
+                  if constexpr (ES == 2 && ACT <= FCM_ACT_RELU6) {
+                    const uint32_t cb = cs.base + 4 * (sl * TD + c0);
 #pragma unroll
-              for (int v = 0; v < ES; ++v) sts128(dst + 16 * v, o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                      const uint4 sc = lds128(cb + 16 * q4), bi = lds128(cb + 4 * cs.ncap + 16 * q4);
+                      const uint32_t* a4 = &rg[16 * hh + 4 * q4];
+                      o[2 * q4] = epi_act2<DT, ACT>(__uint_as_float(a4[0]), __uint_as_float(a4[1]),
+                                                    f2_pack(__uint_as_float(sc.x), __uint_as_float(sc.y)),
+                                                    f2_pack(__uint_as_float(bi.x), __uint_as_float(bi.y)), hi_c);
+                      o[2 * q4 + 1] = epi_act2<DT, ACT>(__uint_as_float(a4[2]), __uint_as_float(a4[3]),
+                                                        f2_pack(__uint_as_float(sc.z), __uint_as_float(sc.w)),
+                                                        f2_pack(__uint_as_float(bi.z), __uint_as_float(bi.w)), hi_c);
+                    }
+                  } else {
+                    epi16_any<DT>(&rg[16 * hh], cs, ep, sl * TD + c0, o, false, uint4{}, uint4{});
+                  }
+                }
+                const uint32_t dst = smem_u32(tb) + r * PITCH + c0 * ES;
+#pragma unroll
+                for (int v = 0; v < ES; ++v) sts128(dst + 16 * v, o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+              }
             }
           }
         }
+      };
+      if constexpr (ES == 2) {
+        if (ep.act == FCM_ACT_RELU6) produce(std::integral_constant<int, FCM_ACT_RELU6>());
+        else if (ep.act == FCM_ACT_RELU) produce(std::integral_constant<int, FCM_ACT_RELU>());
+        else if (ep.act == FCM_ACT_NONE) produce(std::integral_constant<int, FCM_ACT_NONE>());
+        else produce(std::integral_constant<int, 99>());
+      } else {
+        produce(std::integral_constant<int, 99>());
       }
       tc_fence_before();
       mbar_arrive(Tfull + acc);
@@ -1167,12 +1228,19 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       if constexpr (kPair) {
         // column-pair FFMA2 core (as in DWPW): a lane owns one channel word of 2 adjacent output
         // columns x SEG rows; stores go straight to the NHWC OFM (128 B per warp and pixel)
+        // lane groups: a partly filled last slice (C_mid not a multiple of 64) packs 2 or 4 items
+        // into one warp (slots of 16 / 8 lanes) instead of computing idle channel words
+        const int cw_valid = min(32, (Cmid - sl * TD) / V);
+        const int gi = cw_valid > 16 ? 0 : (cw_valid > 8 ? 1 : 2);
+        const int gsl = 5 - gi, grp = lane >> gsl, wd = lane & ((1 << gsl) - 1);
         if (sl != sl_w) {  // this slice's weights / scale / bias (once per CTA with resident slices)
-          load_dw3_h(wsm, nslice * 32, sl * 32 + lane, W9, sc2, bi2);
+          load_dw3_h(wsm, nslice * 32, sl * 32 + wd, W9, sc2, bi2);
           sl_w = sl;
         }
-        const bool cval = c < Cmid;
-        const int hp = (tw + 1) >> 1;
+        const int cw = sl * TD + wd * V;
+        const bool cval = cw < Cmid;
+        constexpr int NC = kDwpwNC;
+        const int hp = (tw + NC - 1) / NC;
         group_wait(Tfull + tbi, (local / depth) & 1, dw == 0, 3, kPwdwNDW * 32);
         if (dw == 0 && lane == 0) stamp(local, 6);
         {
@@ -1181,23 +1249,24 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
             constexpr int ACT = decltype(actc)::value;
             const int nsg = (th + SEG - 1) / SEG;
             const int nit = nb * hp * nsg;
-            for (int item = dw; item < nit && !(dbg & 1); item += kPwdwNDW) {
-              // ragged last segment / odd last column pair shifted back inside the tile (SEG <= th):
-              // the overlap is recomputed and stored twice with identical values
+            for (int base = dw << gi; base < nit && !(dbg & 1); base += kPwdwNDW << gi) {
+              const int item = base + grp;
+              if (item >= nit) continue;
+              // ragged last segment / column group shifted back inside the tile (SEG <= th): the
+              // overlap is recomputed and stored twice with identical values
               const int cp = fdiv(item, dv.nsg), seg = item - cp * nsg;
               const int b = fdiv(cp, dv.hp);
-              const int x0 = max(0, min(2 * (cp - b * hp), tw - 2));
+              const int x0 = max(0, min(NC * (cp - b * hp), tw - NC));
               const int n = nbi * nb + b, xo = txi * tw + x0;
               const int y0 = min(seg * SEG, th - SEG);
               if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
-              const uint32_t src = tsa + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * PW + lane) * 4;
+              const uint32_t src = tsa + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * PW + wd) * 4;
               const int nvalid = nrows_t - y0;
-              const bool c0ok = cval, c1ok = cval && (x0 + 1 < tw) && (xo + 1 < Wo);
-              uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + c) / V;
+              const int ncv = cval ? min(min(NC, tw - x0), Wo - xo) : 0;  // columns stored
+              uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + cw) / V;
               const size_t rstride = (size_t)Wo * Cmid / V, cstride = (size_t)Cmid / V;
-              dw3_cols_roll<DT, S, 2, PITCH>(src, tw_in * PITCH, SEG, W9, [&](int r, int cc, float lo, float hi) {
-                if (r < nvalid && (cc == 0 ? c0ok : c1ok))
-                  dst[r * rstride + cc * cstride] = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
+              dw3_cols_roll<DT, S, NC, PITCH>(src, tw_in * PITCH, SEG, W9, [&](int r, int cc, float lo, float hi) {
+                if (r < nvalid && cc < ncv) dst[r * rstride + cc * cstride] = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
               });
             }
           });
@@ -1369,7 +1438,7 @@ int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, 
 // the fewest input rows per DW warp (rounds x rows per item, + 2 rows of per-item overhead).
 template <int K, int S>
 static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
-  const int hp = (g.tw + 1) / 2;
+  const int hp = (g.tw + kDwpwNC - 1) / kDwpwNC;  // column groups per image row (pair core)
   int sel = 0;
   DwDivs d{};
   for (int gi = 0; gi < 3; ++gi) {
@@ -1448,10 +1517,13 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   int XS = std::min(xs_cap, (smem_cap - fixed - BS * BN * 128) / xstride);
   if (XS < 2) return set_error(FCM_E_INFEASIBLE, "dwpw: tile too large for 2 X stages");
   // resident weights: grid a multiple of nsplit fixes each CTA's C_out slice; keep all nk chunks
-  // when that costs at most one X stage (and leaves >= 2)
+  // unless that leaves fewer than min(XS, kXsMin) X stages: the X halo chunk is the latency-critical
+  // load (a 14 x 14 x 64-channel box takes ~1-2.5k cycles to land; with 2 stages in flight the DW
+  // phases wait on it), the weights are L2 hits either way
+  static const int xs_min = [] { const char* e = getenv("FCM_XS_MIN"); return e ? atoi(e) : 4; }();
   const int resgrid = (grid / nsplit) * nsplit;
   const int xs_res = std::min(xs_cap, (smem_cap - fixed - nk * BN * 128) / xstride);
-  const bool resB = nk <= 16 && resgrid > 0 && resgrid >= grid * 15 / 16 && xs_res >= 2 && xs_res >= XS - 1;
+  const bool resB = nk <= 16 && resgrid > 0 && resgrid >= grid * 15 / 16 && xs_res >= 2 && xs_res >= std::min(XS, xs_min);
   if (resB) {
     grid = resgrid;
     BS = nk;
@@ -1462,6 +1534,10 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   using TT = typename Tr<DT>::T;
   DwDivs dv = dwpw_divs<K, S>(g, dwpw_ndw<DT, K>(), nsplit);
+  static const bool verbose = getenv("FCM_VERBOSE") != nullptr;  // development: launch configuration
+  if (verbose)
+    fprintf(stderr, "dwpw: grid %d XS %d BS %d resB %d BN %d nsplit %d MB %d seg_sel %06x smem %zu\n", grid, XS, BS,
+            (int)resB, BN, nsplit, MB, dv.seg_sel, smem);
   launch_k(kern, dim3(grid), dim3((4 + dwpw_ndw<DT, K>() + 4) * 32), smem, st, tx, tb, y, static_cast<const TT*>(wdw), ed, ep, g.N, g.C,
                                                               g.Ho, g.Wo, g.Cout, g.pt, g.pl, g.nb, g.th, g.tw,
                                                               tiles_x, tiles_y, nsplit, BN, XS, BS,
@@ -1495,8 +1571,8 @@ int launch_dwpw_tc(int dt, const void* x, const void* wdw, const Epi& ed, const 
 // PWDW_R tile decode + DW item decode; the pair core's segment length is the one with the fewest
 // input rows per DW warp (rounds x rows per item, + 2 rows of per-item overhead).
 template <int DT, int K, int S>
-static PwdwDivs pwdw_divs(const Geo& g, int nslice, int tiles_x, int tiles_y) {
-  const int hp = (g.tw + 1) / 2;
+static PwdwDivs pwdw_divs(const Geo& g, int nslice, int tiles_x, int tiles_y, int grid, int resB) {
+  const int hp = (g.tw + kDwpwNC - 1) / kDwpwNC;
   int best = 1, bcost = 1 << 30;
   for (int seg = std::min(g.th, 32); seg >= 1; --seg) {  // any length (rolled core); ragged ones shift up
     const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
@@ -1506,7 +1582,9 @@ static PwdwDivs pwdw_divs(const Geo& g, int nslice, int tiles_x, int tiles_y) {
   }
   return PwdwDivs{make_fdiv(nslice), make_fdiv(tiles_x), make_fdiv(tiles_y), make_fdiv(g.tw),
                   make_fdiv((g.th + pwdw_seg<DT, K, S>() - 1) / pwdw_seg<DT, K, S>()), make_fdiv(hp),
-                  make_fdiv((g.th + best - 1) / best), best};
+                  make_fdiv((g.th + best - 1) / best), best,
+                  make_fdiv(((g.th - 1) * S + K) * ((g.tw - 1) * S + K)), make_fdiv((g.tw - 1) * S + K),
+                  make_fdiv(resB == 2 ? (1 << 30) : std::max(1, grid / nslice))};
 }
 
 template <int DT, int K, int S>
@@ -1517,14 +1595,18 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   constexpr int TD = 128 / ES;
   const int th_in = (g.th - 1) * S + K, tw_in = (g.tw - 1) * S + K;
   const int R = g.nb * th_in * tw_in;
-  if (R > 256) return set_error(FCM_E_INFEASIBLE, "pwdw_r: halo tile has more than 256 pixels");
+  if (R > 512) return set_error(FCM_E_INFEASIBLE, "pwdw_r: halo tile has more than 512 pixels");
   const int MB = (R + 127) / 128;
+  // X box width: the pixel's C_in bytes rounded up to 32 / 64, else 128-byte channel chunks
+  const int xb = g.C * ES <= 32 ? 32 : (g.C * ES <= 64 ? 64 : 128);
   CUtensorMap tx, tb;
   {
     const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
     const uint64_t str[3] = {(uint64_t)g.C * ES, (uint64_t)g.W * g.C * ES, (uint64_t)g.H * g.W * g.C * ES};
-    const uint32_t box[4] = {(uint32_t)KC, (uint32_t)tw_in, (uint32_t)th_in, (uint32_t)g.nb};
-    if (!encode_tmap(&tx, tmap_dtype(DT), 4, x, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+    const uint32_t box[4] = {(uint32_t)(xb / ES), (uint32_t)tw_in, (uint32_t)th_in, (uint32_t)g.nb};
+    const CUtensorMapSwizzle sw = xb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                            : (xb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    if (!encode_tmap(&tx, tmap_dtype(DT), 4, x, dims, str, box, sw))
       return set_error(FCM_E_CUDA, "tensor map (PWDW X) failed");
   }
   {
@@ -1543,10 +1625,12 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   const int total = ((g.N + g.nb - 1) / g.nb) * tiles_x * tiles_y * nslice;
   int grid = std::min(total, device_props().sms);
-  // resident weights (as in the LBL PW): with the grid a multiple of nslice each CTA's C_mid slice
-  // is fixed, so its nk weight chunks are loaded once instead of once per tile by every CTA
-  auto plan = [&](bool res, int& stages, int& dep) {
-    const int sb = MB * 16384 + (res ? 0 : TD * 128), extra = res ? nk * TD * 128 : 0;
+  // resident weights: all nk x nslice weight tiles loaded once per CTA when they take <= 64 KB and
+  // fit (mode 1); else this CTA's own slice with the grid a multiple of nslice (mode 2); else one
+  // B tile per X stage
+  auto plan = [&](int res, int& stages, int& dep) {
+    const int sb = MB * 128 * xb + (res ? 0 : TD * 128);
+    const int extra = res == 1 ? nk * nslice * TD * 128 : (res == 2 ? nk * TD * 128 : 0);
     for (dep = depth; dep >= 2; --dep) {
       stages = std::min(4, (device_props().smem_optin - fixed - extra - dep * tbytes) / sb);
       if (stages >= 2) return (size_t)fixed + extra + (size_t)dep * tbytes + (size_t)stages * sb;
@@ -1555,14 +1639,16 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
     return (size_t)0;
   };
   int stages = 0, dep = 0;
+  int resB = 0;
+  size_t smem = 0;
   const int resgrid = (grid / nslice) * nslice;
-  bool resB = resgrid > 0 && resgrid >= grid * 15 / 16;
-  size_t smem = resB ? plan(true, stages, dep) : 0;
-  if (resB && stages >= 2) {
+  if (nk * nslice * TD * 128 <= 64 * 1024 && (smem = plan(1, stages, dep)) && stages >= 2) {
+    resB = 1;
+  } else if (resgrid > 0 && resgrid >= grid * 15 / 16 && (smem = plan(2, stages, dep)) && stages >= 2) {
+    resB = 2;
     grid = resgrid;
   } else {
-    resB = false;
-    smem = plan(false, stages, dep);
+    smem = plan(0, stages, dep);
   }
   if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pwdw_r: tile too large for 2 smem stages");
   auto kern = pwdw_tc_kernel<DT, K, S>;
@@ -1571,8 +1657,8 @@ static int launch_pwdw_t(const void* x, const void* wp, const Epi& ep, const voi
   launch_k(kern, dim3(grid), dim3((pwdw_ntp<K>() + kPwdwNDW + 2) * 32), smem, st, tx, tb, static_cast<const TT*>(wdw), ep, ed,
                                                      static_cast<uint8_t*>(y), g.N, g.H, g.W, g.C, g.Ho, g.Wo, g.Cout,
                                                      g.pt, g.pl, g.nb, g.th, g.tw, tiles_x, tiles_y, stages, dep,
-                                                     pow2_cols(dep * MB * TD), ncap, resB ? 1 : 0,
-                                                     pwdw_divs<DT, K, S>(g, nslice, tiles_x, tiles_y),
+                                                     pow2_cols(dep * MB * TD), ncap, resB,
+                                                     pwdw_divs<DT, K, S>(g, nslice, tiles_x, tiles_y, grid, resB), xb,
                                                      debug_flags(), trace_buf());
   const int rc = check_launch("pwdw_tc_kernel");
   trace_dump("pwdw");

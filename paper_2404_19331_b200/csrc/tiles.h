@@ -99,9 +99,11 @@ inline long pwdw_tile_cost(const Geo& g, int nb, int th, int tw) {
   return tiles * ((long)nb * th_in * tw_in + nb * th * tw + 32);
 }
 
-inline bool pwdw_tile_ok(const Geo& g, int nb, int th, int tw) {
+// rmax: MMA rows of the halo tile the default / planner tiles use (the kernel takes up to 512 for
+// bf16 / f16: 4 row blocks x 64 T columns x 2 TMEM buffers; measured plans search those)
+inline bool pwdw_tile_ok(const Geo& g, int nb, int th, int tw, int rmax = 256) {
   const int th_in = halo(th, g.k, g.s), tw_in = halo(tw, g.k, g.s);
-  return nb * th_in * tw_in <= 256 && th_in <= 256 && tw_in <= 256;
+  return nb * th_in * tw_in <= rmax && th_in <= 256 && tw_in <= 256;
 }
 
 // Shared memory of the tensor-core PWDW_R kernel at its minimum configuration (2 X/B stages, 2 T
@@ -117,7 +119,8 @@ inline bool pwdw_smem_fits(int dt, const Geo& g, int smem_optin = 232448) {
   const bool pair = (dt == FCM_BF16 || dt == FCM_F16) && g.k == 3;
   const long wbytes = pair ? 52 * nslice * 32 : (long)g.k * g.k * nslice * 128;  // dw3h_bytes
   const long fixed = 1024 + 2 * consts + wbytes + 512;
-  return fixed + 2 * tbytes + 2 * (mb * 16384 + td * 128) <= smem_optin;
+  const long xb = (long)g.C * es <= 32 ? 32 : ((long)g.C * es <= 64 ? 64 : 128);  // X box bytes / pixel
+  return 2 * mb * td <= 512 && fixed + 2 * tbytes + 2 * (mb * 128 * xb + td * 128) <= smem_optin;
 }
 
 inline void default_pwdw_tile(Geo& g) {

@@ -127,6 +127,30 @@ def test_pwdw_r_tiling_invariance_bitwise():
         assert np.array_equal(o, outs[0])
 
 
+# halo tiles of up to 512 MMA rows (4 row blocks; bf16 / f16) and X boxes staged at the pixel's own
+# width (C_in * 2 bytes rounded to 32 / 64, else 128-byte chunks), 4-column DW items incl. tiles
+# narrower than 4 columns and ragged maps
+@pytest.mark.parametrize("fmt", ["bf16", "f16"])
+@pytest.mark.parametrize("c_in,s,h,w,tile", [
+    (16, 2, 37, 45, dict(tile_h=7, tile_w=14)),    # R = 15 x 29 = 435, 32-byte X rows
+    (24, 2, 33, 30, dict(tile_h=8, tile_w=14)),    # R = 17 x 29 = 493, 64-byte X rows
+    (32, 1, 29, 31, dict(tile_h=14, tile_w=28)),   # R = 16 x 30 = 480
+    (72, 1, 23, 26, dict(tile_h=16, tile_w=16)),   # R = 324 (3 row blocks), two C_in chunks (64 + 8)
+    (16, 1, 13, 11, dict(tile_h=13, tile_w=3)),    # tile narrower than a 4-column DW item
+    (40, 2, 21, 9, dict(tile_h=5, tile_w=2)),
+])
+def test_pwdw_r_wide_halo_narrow_x(fmt, c_in, s, h, w, tile):
+    Case("pwdw", fmt, 2, h, w, c_in, 96, k=3, s=s, tile=tile).check()
+
+
+def test_pwdw_r_wide_halo_tiling_invariance_bitwise():
+    outs = []
+    for tile in [dict(tile_h=4, tile_w=4), dict(tile_h=7, tile_w=14), dict(tile_h=8, tile_w=14), dict(tile_h=15, tile_w=3)]:
+        outs.append(Case("pwdw", "bf16", 2, 30, 29, 16, 96, k=3, s=2, tile=tile).gpu())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
 # ---------------------------------------------------------------- GPU self-consistency
 def test_int8_fused_equals_unfused_bitwise():
     import paper_2404_19331_b200 as fcm

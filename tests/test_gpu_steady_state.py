@@ -67,6 +67,16 @@ def test_pwdw_r_steady_state(fmt, s):
     Case("pwdw", fmt, n, h, h, c_in, c_mid, k=3, s=s, tile=tile).check()
 
 
+@pytest.mark.parametrize("fmt", ["bf16", "f16"])
+def test_pwdw_r_wide_halo_steady_state(fmt):
+    # 7 x 14 stride-2 output tiles (435 halo rows = 4 MMA row blocks), 32-byte X rows (C_in = 16)
+    tile = dict(tile_h=7, tile_w=14)
+    ho, wo = 28, 28
+    n = math.ceil(3 * SMS / (_tiles(1, ho, wo, tile) * 2))
+    assert _tiles(n, ho, wo, tile, 2) >= 3 * SMS
+    Case("pwdw", fmt, n, 2 * ho, 2 * wo, 16, 96, k=3, s=2, tile=tile).check()
+
+
 @pytest.mark.parametrize("fmt", ["bf16", "f16", "s8"])
 @pytest.mark.parametrize("c_in,c_out", [(64, 96), (144, 24), (96, 576)])
 def test_pw_steady_state(fmt, c_in, c_out):
