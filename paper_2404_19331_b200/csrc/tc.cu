@@ -955,6 +955,7 @@ struct PwdwDivs {
   int seg;                        // pair core segment length
   FDiv thw_in, tw_in;             // T producers: halo row r -> (image, row, column)
   FDiv rot;                       // slice rotation period (spatial tiles per round of the grid)
+  int nsgi;                       // ceil(th / seg)
 };
 template <int DT, int K> constexpr bool pwdw_pair() { return (DT == FCM_BF16 || DT == FCM_F16) && K == 3; }
 template <int DT, int K> constexpr int pwdw_wbytes(int nslice) {
@@ -1127,15 +1128,16 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     constexpr int NU = CPW / 32;    // 32-column TMEM loads per M block
     const int q = warp & 3, h = warp >> 2;
     int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const int acc = local % depth;
+    Ring rt(depth);
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local, rt.next()) {
+      const int acc = rt.i;
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       uint8_t* tb = tsm + acc * tbytes;
       if (warp == 0) {
-        mbar_wait(tfull + acc, (local / depth) & 1);
+        mbar_wait(tfull + acc, rt.ph);
         if (lane == 0) stamp(local, 3);
-        mbar_wait(Tempty + acc, ((local / depth) & 1) ^ 1);
+        mbar_wait(Tempty + acc, rt.ph ^ 1);
         if (lane == 0) stamp(local, 4);
       }
       named_bar_sync(2, NTP * 32);
@@ -1216,9 +1218,13 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
     uint32_t W9[9];
     uint64_t sc2 = 0ull, bi2 = 0ull;
     int sl_w = -1;
+    // the activation is dispatched once for the whole role (not per tile)
+    auto role = [&](auto actc) {
+    constexpr int ACT = decltype(actc)::value;
+    Ring rt(depth);
     int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const int tbi = local % depth;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local, rt.next()) {
+      const int tbi = rt.i;
       int sl, nbi, tyi, txi;
       decode(t, sl, nbi, tyi, txi);
       const int c = sl * TD + lane * V;
@@ -1226,7 +1232,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       const int y0t = tyi * th;
       const int nrows_t = min(th, Ho - y0t);
       if constexpr (kPair) {
-        // column-pair FFMA2 core (as in DWPW): a lane owns one channel word of 2 adjacent output
+        // column-group core (as in DWPW): a lane owns one channel word of NC adjacent output
         // columns x SEG rows; stores go straight to the NHWC OFM (128 B per warp and pixel)
         // lane groups: a partly filled last slice (C_mid not a multiple of 64) packs 2 or 4 items
         // into one warp (slots of 16 / 8 lanes) instead of computing idle channel words
@@ -1241,34 +1247,29 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
         const bool cval = cw < Cmid;
         constexpr int NC = kDwpwNC;
         const int hp = (tw + NC - 1) / NC;
-        group_wait(Tfull + tbi, (local / depth) & 1, dw == 0, 3, kPwdwNDW * 32);
+        group_wait(Tfull + tbi, rt.ph, dw == 0, 3, kPwdwNDW * 32);
         if (dw == 0 && lane == 0) stamp(local, 6);
-        {
-          const int SEG = dv.seg;  // rows per item (runtime, rolled core)
-          with_act(ed.act, [&](auto actc) {
-            constexpr int ACT = decltype(actc)::value;
-            const int nsg = (th + SEG - 1) / SEG;
-            const int nit = nb * hp * nsg;
-            for (int base = dw << gi; base < nit && !(dbg & 1); base += kPwdwNDW << gi) {
-              const int item = base + grp;
-              if (item >= nit) continue;
-              // ragged last segment / column group shifted back inside the tile (SEG <= th): the
-              // overlap is recomputed and stored twice with identical values
-              const int cp = fdiv(item, dv.nsg), seg = item - cp * nsg;
-              const int b = fdiv(cp, dv.hp);
-              const int x0 = max(0, min(NC * (cp - b * hp), tw - NC));
-              const int n = nbi * nb + b, xo = txi * tw + x0;
-              const int y0 = min(seg * SEG, th - SEG);
-              if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
-              const uint32_t src = tsa + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * PW + wd) * 4;
-              const int nvalid = nrows_t - y0;
-              const int ncv = cval ? min(min(NC, tw - x0), Wo - xo) : 0;  // columns stored
-              uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + cw) / V;
-              const size_t rstride = (size_t)Wo * Cmid / V, cstride = (size_t)Cmid / V;
-              dw3_cols_roll<DT, S, NC, PITCH>(src, tw_in * PITCH, SEG, W9, [&](int r, int cc, float lo, float hi) {
-                if (r < nvalid && cc < ncv) dst[r * rstride + cc * cstride] = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
-              });
-            }
+        const int SEG = dv.seg, nsg = dv.nsgi;  // rows per item (runtime, rolled core), segments
+        const int nit = nb * hp * nsg;
+        const uint32_t rstride = (uint32_t)Wo * Cmid / V, cstride = (uint32_t)Cmid / V;
+        for (int base = dw << gi; base < nit && !(dbg & 1); base += kPwdwNDW << gi) {
+          const int item = base + grp;
+          if (item >= nit) continue;
+          // ragged last segment / column group shifted back inside the tile (SEG <= th): the
+          // overlap is recomputed and stored twice with identical values
+          const int cp = fdiv(item, dv.nsg), seg = item - cp * nsg;
+          const int b = fdiv(cp, dv.hp);
+          const int x0 = max(0, min(NC * (cp - b * hp), tw - NC));
+          const int n = nbi * nb + b, xo = txi * tw + x0;
+          const int y0 = min(seg * SEG, th - SEG);
+          if (n >= N || xo >= Wo || y0 >= nrows_t) continue;
+          const uint32_t src = tsa + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * PW + wd) * 4;
+          const int nvalid = nrows_t - y0;
+          const int ncv = cval ? min(min(NC, tw - x0), Wo - xo) : 0;  // columns stored
+          uint32_t* dst = yw + ((((size_t)n * Ho + (y0t + y0)) * Wo + xo) * Cmid + cw) / V;
+          dw3_cols_roll<DT, S, NC, PITCH>(src, tw_in * PITCH, SEG, W9, [&](int r, int cc, float lo, float hi) {
+            if (r < nvalid && cc < ncv)
+              dst[(uint32_t)r * rstride + (uint32_t)cc * cstride] = epi_act2<DT, ACT>(lo, hi, sc2, bi2, hi_c);
           });
         }
       } else {
@@ -1277,7 +1278,7 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
         EpiC ec[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) ec[v] = epic<DT>(dcs, c + v);
-        group_wait(Tfull + tbi, (local / depth) & 1, dw == 0, 3, kPwdwNDW * 32);
+        group_wait(Tfull + tbi, rt.ph, dw == 0, 3, kPwdwNDW * 32);
         for (int item = dw; item < nitems; item += kPwdwNDW) {
           const int col = fdiv(item, dv.nseg), seg = item - col * nseg;
           const int b = fdiv(col, dv.tw), x = col - b * tw;
@@ -1297,6 +1298,9 @@ __global__ void __launch_bounds__((pwdw_ntp<K>() + kPwdwNDW + 2) * 32, 1)
       mbar_arrive(Tempty + tbi);
       if (dw == 0 && lane == 0) stamp(local, 7);
     }
+    };
+    if constexpr (kPair) with_act(ed.act, role);
+    else role(std::integral_constant<int, 0>());
   }
   __syncthreads();
   if (warp == WARP_MMA) {
@@ -1584,7 +1588,7 @@ static PwdwDivs pwdw_divs(const Geo& g, int nslice, int tiles_x, int tiles_y, in
                   make_fdiv((g.th + pwdw_seg<DT, K, S>() - 1) / pwdw_seg<DT, K, S>()), make_fdiv(hp),
                   make_fdiv((g.th + best - 1) / best), best,
                   make_fdiv(((g.th - 1) * S + K) * ((g.tw - 1) * S + K)), make_fdiv((g.tw - 1) * S + K),
-                  make_fdiv(resB == 2 ? (1 << 30) : std::max(1, grid / nslice))};
+                  make_fdiv(resB == 2 ? (1 << 30) : std::max(1, grid / nslice)), (g.th + best - 1) / best};
 }
 
 template <int DT, int K, int S>
