@@ -714,6 +714,13 @@ __device__ __forceinline__ void with_act(int act, F&& f) {
   else f(std::integral_constant<int, 0>());
 }
 
+// with_act, or the RELU6 variant alone when the kernel is compiled for it
+template <bool R6, class F>
+__device__ __forceinline__ void with_act_r6(int act, F&& f) {
+  if constexpr (R6) f(std::integral_constant<int, 2>());
+  else with_act(act, static_cast<F&&>(f));
+}
+
 // fp32 pair (lo, hi) -> folded-BN affine (one FFMA2) -> packed bf16x2 / f16x2 with the activation
 template <int DT, int ACT>
 __device__ __forceinline__ uint32_t epi_act2(float lo, float hi, uint64_t sc2, uint64_t bi2, uint32_t hi_c) {
