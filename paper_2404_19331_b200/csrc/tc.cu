@@ -59,7 +59,8 @@ __device__ __forceinline__ float2 word2f(uint32_t w) {
 // call, so a kernel only fetches the code it runs (the DWPW epilogue shares the SM's instruction
 // cache with the DW stage's hot loop; measured: a per-element activation switch with erf inlined 16x
 // cost the DW warps 2x in instruction-fetch stalls).
-template <int DT, bool RES = false>
+// SMOOTH = false: the kernel is compiled for NONE / RELU / RELU6 only (no SiLU / GELU code)
+template <int DT, bool RES = false, bool SMOOTH = true>
 __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
                                       uint32_t (&out)[8], uint4 ra = uint4{}, uint4 rb = uint4{}) {
   if constexpr (DT == FCM_S8) {
@@ -89,7 +90,7 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
       bi[4 * q] = __uint_as_float(b.x); bi[4 * q + 1] = __uint_as_float(b.y);
       bi[4 * q + 2] = __uint_as_float(b.z); bi[4 * q + 3] = __uint_as_float(b.w);
     }
-    if (e.act > FCM_ACT_RELU6) {
+    if (SMOOTH && e.act > FCM_ACT_RELU6) {
       // SiLU / GELU (+ residual): the activation dispatched once per call (one variant's code is
       // fetched; a rolled loop would move r / out to local memory)
       with_act(e.act, [&](auto actc) {
@@ -136,14 +137,14 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
 
 // One 16-column epilogue step of a float (bf16 / f16) output with the runtime activation / residual
 // choice; r points at 16 consecutive accumulator words.
-template <int DT>
+template <int DT, bool SMOOTH = true>
 __device__ __forceinline__ void epi16_any(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
                                           uint32_t (&out)[8], bool res, uint4 ra, uint4 rb) {
   if constexpr (DT == FCM_S8) {
     epi16<DT>(r, cs, e, n_base, out);
   } else {
-    if (res) epi16<DT, true>(r, cs, e, n_base, out, ra, rb);
-    else epi16<DT>(r, cs, e, n_base, out);
+    if (res) epi16<DT, true, SMOOTH>(r, cs, e, n_base, out, ra, rb);
+    else epi16<DT, false, SMOOTH>(r, cs, e, n_base, out);
   }
 }
 
@@ -468,9 +469,10 @@ template <int DT, int K> constexpr int dwpw_wbytes(int nk) {
   return dwpw_pair<DT, K>() ? dw3h_bytes(nk * 32) : K * K * nk * 32 * 4;
 }
 
-// R6: the DW activation is RELU6 (one compiled DW epilogue variant: measured 7 % faster DWPW on
-// MobileNetV2 b2 than the runtime five-way dispatch, whose variants share the instruction cache with
-// the other warp roles); otherwise the activation is dispatched at run time
+// R6: the DW activation is RELU6 and the PW one NONE / RELU / RELU6 (one compiled DW epilogue
+// variant, no SiLU / GELU code in the PW epilogue: measured 7 % faster DWPW on MobileNetV2 b2 than
+// the runtime dispatch, whose variants share the instruction cache with the other warp roles);
+// otherwise the activations are dispatched at run time
 template <int DT, int K, int S, bool R6 = false>
 __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     dwpw_tc_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmb,
@@ -906,7 +908,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             tmem_ld_wait();
             uint32_t o[8];
             // (the residual: the shortcut input at the same NHWC position)
-            epi16_any<DT>(r, cs, ep, ns * BN + cb, o, hasres, rcur.v[2 * hh], rcur.v[2 * hh + 1]);
+            epi16_any<DT, !R6>(r, cs, ep, ns * BN + cb, o, hasres, rcur.v[2 * hh], rcur.v[2 * hh + 1]);
             if (ok) {
               if constexpr (ES == 2) {
                 stg128(dst + cb * 2, o[0], o[1], o[2], o[3]);
@@ -1541,7 +1543,7 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   const size_t smem = (size_t)fixed + (size_t)BS * BN * 128 + (size_t)XS * xstride;
   auto kern = dwpw_tc_kernel<DT, K, S>;
   if constexpr (dwpw_pair<DT, K>())
-    if (ed.act == FCM_ACT_RELU6) kern = dwpw_tc_kernel<DT, K, S, true>;
+    if (ed.act == FCM_ACT_RELU6 && ep.act <= FCM_ACT_RELU6) kern = dwpw_tc_kernel<DT, K, S, true>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   using TT = typename Tr<DT>::T;
   DwDivs dv = dwpw_divs<K, S>(g, dwpw_ndw<DT, K>(), nsplit);
