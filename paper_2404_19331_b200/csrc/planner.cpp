@@ -41,7 +41,12 @@ struct Layer {
 
 struct Gpu {
   ll sms = 148, smem = 232448, l2 = 126LL << 20;
-  double hbm_gbs = 6534.5, l2_gbs = 20000, tc_tmacs = 832, ffma_tmacs = 37.2, dw_eff = 0.5, launch_us = 2.0;
+  // calibrated on B200 against the measured per-launch times of the MobileNetV2 bf16 b256 plan
+  // (profiles/r02/layers.json, tests/test_planner_time_model.py): the kernels reach ~0.5 of the HBM
+  // peak on their compulsory bytes, the bf16 DW stage ~0.16 of the FFMA peak, each PWDW_R T value
+  // (PW output over the halo: TMEM -> epilogue -> smem) costs about 2 DW MACs, ~8 us per launch
+  double hbm_gbs = 6534.5, l2_gbs = 20000, tc_tmacs = 832, ffma_tmacs = 37.2, dw_eff = 0.16, launch_us = 8.0;
+  double hbm_eff = 0.5, t_cost = 2.0;
   // int8 DW efficiency (of the FFMA peak), measured on B200: LBL FFMA2 core ~0.17, inside the fused
   // kernels ~0.085 (profiles/r01_ncu_summary.md)
   double dw_eff_i8 = 0.17, dw_eff_i8_fused = 0.085;
@@ -224,7 +229,7 @@ struct Cost {
   bool ok = false;
   std::string op;
   double us = 0;
-  ll dram = 0, l2 = 0, dw_macs = 0, pw_macs = 0, red_macs = 0;
+  ll dram = 0, l2 = 0, dw_macs = 0, pw_macs = 0, red_macs = 0, t_vals = 0;
   ll nb = 1, th = 0, tw = 0, nsplit = 0;
   ll gma = -1, p_th = 0, p_tw = 0, p_td = 0;  // paper mode: Eq. value (bytes) and its argmin tile
   // paper mode keeps the paper's decision even for a pair the fused kernels cannot run
@@ -234,10 +239,10 @@ struct Cost {
 };
 
 static double t_us(const Cost& c, int dt, const Gpu& g) {
-  const double hbm = c.dram / (g.hbm_gbs * 1e3);
+  const double hbm = c.dram / (g.hbm_gbs * g.hbm_eff * 1e3);
   const double l2 = c.l2 / (g.l2_gbs * 1e3);
   const double eff = dt == FCM_S8 ? (c.op == "dw" ? g.dw_eff_i8 : g.dw_eff_i8_fused) : g.dw_eff;
-  const double dw = c.dw_macs / (g.ffma_tmacs * 1e6 * eff);
+  const double dw = (c.dw_macs + g.t_cost * c.t_vals) / (g.ffma_tmacs * 1e6 * eff);
   const double tcr = (dt == FCM_F32) ? g.ffma_tmacs : (dt == FCM_S8 ? 2.0 : 1.0) * g.tc_tmacs;
   const double pw = c.pw_macs / (tcr * 1e6);
   return std::max(std::max(hbm, l2), std::max(dw, pw)) + g.launch_us;
@@ -338,6 +343,7 @@ static Cost b200_pwdw(const Layer& p, const Layer& d, ll N, int dt, ll b, const 
   c.dram = (N * (d.H * d.W * Cin + d.Ho * d.Wo * Cm) + Cin * Cm + d.k * d.k * Cm) * b;
   c.dw_macs = N * d.Ho * d.Wo * Cm * d.k * d.k;
   c.pw_macs = u.halo * Cin;
+  c.t_vals = u.halo;  // T values produced over the halo tiles (epilogue + smem writes)
   c.red_macs = (u.halo - N * d.H * d.W * Cm) * Cin;
   if (g.th == d.Ho && g.tw == d.Wo) c.op = "pwdw";
   c.us = t_us(c, dt, gp);
@@ -436,6 +442,8 @@ static std::string run(const char* model_json, const char* gpu_json) {
     gp.dw_eff_i8 = g.num("dw_eff_i8", gp.dw_eff_i8);
     gp.dw_eff_i8_fused = g.num("dw_eff_i8_fused", gp.dw_eff_i8_fused);
     gp.launch_us = g.num("launch_us", gp.launch_us);
+    gp.hbm_eff = g.num("hbm_eff", gp.hbm_eff);
+    gp.t_cost = g.num("t_cost", gp.t_cost);
   }
   const Value* lv = m.get("layers");
   if (!lv || lv->kind != Value::Arr || lv->a.empty()) throw std::runtime_error("model needs a non-empty layers array");
