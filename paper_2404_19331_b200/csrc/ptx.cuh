@@ -174,6 +174,13 @@ __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool 
   named_bar_sync(bar_id, nthreads);
 }
 
+// group_wait whose leader backs off between polls (a phase that is usually far away)
+__device__ __forceinline__ void group_wait_sleep(uint64_t* bar, uint32_t parity, bool leader, uint32_t bar_id,
+                                                 uint32_t nthreads) {
+  if (leader) mbar_wait_sleep<128>(bar, parity);
+  named_bar_sync(bar_id, nthreads);
+}
+
 // ------------------------------------------------------------------ tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // whole warp

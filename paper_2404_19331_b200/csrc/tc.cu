@@ -460,6 +460,7 @@ constexpr int kDwpwNA = 2;  // default A-operand (commBuffer) ring depth
 struct DwDivs {
   FDiv hp;              // column pairs per image
   FDiv nsg[3];          // ceil(th / SEG) for the SEG of each lane-group width
+  int nsgi;             // the same counts, byte gi (<= 255)
   FDiv nsplit, tx, ty;  // tile decode
   FDiv thw, tw;         // epilogue: MMA row m -> (image, row, col) of the tile
   int seg_sel;          // SEG per lane-group width: byte g (g = 0, 1, 2 for 32, 16, 8 lanes per slot)
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
         int ns, nbi, tyi, txi;
         decode(t, ns, nbi, tyi, txi);
         for (int kc = 0; kc < nk; ++kc, rx.next()) {
-          mbar_wait(emptyX + rx.i, rx.ph ^ 1);
+          mbar_wait_sleep<128>(emptyX + rx.i, rx.ph ^ 1);
           if (kc == 0) stamp(local, 8);
           if (kc == nk - 1) stamp(local, 9);
           if (dbg & 8) {  // development: skip the X load (timing attribution only)
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
       for (int t = blockIdx.x; t < total && !resB; t += gridDim.x) {
         const int ns = t - fdiv(t, dv.nsplit) * nsplit;
         for (int kc = 0; kc < nk; ++kc, rb.next()) {
-          mbar_wait(emptyB + rb.i, rb.ph ^ 1);
+          mbar_wait_sleep<128>(emptyB + rb.i, rb.ph ^ 1);
           mbar_arrive_expect_tx(fullB + rb.i, BN * 128);
           tma_load_2d(bbuf + rb.i * BN * 128, &tmb, fullB + rb.i, kc * KC, ns * BN);
         }
@@ -614,13 +615,13 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
       int local = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local, rt.next()) {
         const int acc = rt.i;
-        mbar_wait(tempty + acc, rt.ph ^ 1);
+        mbar_wait_sleep<128>(tempty + acc, rt.ph ^ 1);
         stamp(local, 0);
         tc_fence_after();
         const uint32_t d = tbase + acc * (MB * BN);
         for (int kc = 0; kc < nk; ++kc, ra.next(), rb.next()) {
           const int a = ra.i, sb = resB ? kc : rb.i;
-          mbar_wait(afull + a, ra.ph);
+          mbar_wait_sleep<64>(afull + a, ra.ph);
           cstamp(local * nk + kc, 6);
           if (kc == 0) stamp(local, 1);
           mbar_wait(fullB + sb, resB ? 0 : rb.ph);
@@ -722,7 +723,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             const int SEG = seg_sel;  // rows per item (runtime: the rolled core has one code path)
             with_act_r6<R6>(ed.act, [&](auto actc) {
               constexpr int ACT = decltype(actc)::value;
-              const int nsg = (th + SEG - 1) / SEG;
+              const int nsg = (dv.nsgi >> (8 * gi)) & 0xFF;  // ceil(th / SEG), host-computed
               const int nit = ncp * nsg;
               const uint32_t rstep = (uint32_t)tw * 16;
               for (int base = dw << npl; base < nit && !(dbg & 1); base += kDwpwNDW << npl) {
@@ -883,7 +884,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
       const bool hasres = ES == 2 && ep.residual != nullptr;
       Res32 rnext;
       if (hasres) res32_load(ep.residual, po0, 0, valid, pok0, rnext);
-      group_wait(tfull + acc, rt.ph, warp == 0, 4, 128);
+      group_wait_sleep(tfull + acc, rt.ph, warp == 0, 4, 128);
       if (threadIdx.x == 0) stamp(local, 3);
       tc_fence_after();
       for (int h = 0; h < MB && !(dbg & 2); ++h) {
@@ -1455,7 +1456,7 @@ static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
   for (int gi = 0; gi < 3; ++gi) {
     const int slots = 1 << gi;
     int best = 1, bcost = 1 << 30;
-    for (int seg = std::min(g.th, 32); seg >= 1; --seg) {  // any length (rolled core); ragged ones shift up
+    for (int seg = std::min(g.th, 32); seg >= std::max(1, (g.th + 254) / 255); --seg) {  // any length (rolled core); ragged ones shift up; <= 255 segments (byte field)
       const int nit = g.nb * hp * ((g.th + seg - 1) / seg);
       const int rounds = ((nit + slots - 1) / slots + ndw - 1) / ndw;
       const int cost = rounds * ((seg - 1) * S + K + 2);
@@ -1463,6 +1464,7 @@ static DwDivs dwpw_divs(const Geo& g, int ndw, int nsplit) {
     }
     sel |= best << (8 * gi);
     d.nsg[gi] = make_fdiv((g.th + best - 1) / best);
+    d.nsgi |= ((g.th + best - 1) / best) << (8 * gi);
   }
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
   d.hp = make_fdiv(hp);
