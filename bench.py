@@ -123,7 +123,15 @@ def dist_env():
     return ws, rank, local
 
 
-def kernel_family(op):
+def kernel_family(op, dtype=None, layer=None):
+    """The kernel a plan entry launches. int8 stride-1 3x3 / 5x5 DW layers with a 16-byte pixel pitch
+    on maps >= 14 x 14 (5x5: C <= 512) run the tensor-core DW (the dispatch rule of csrc/dw.cu)."""
+    if op == "dw" and dtype == "s8" and layer is not None:
+        k, s, c = layer["k"], layer["stride"], layer["c"]
+        ho = (layer["h"] + 2 * (k // 2) - k) // s + 1
+        wo = (layer["w"] + 2 * (k // 2) - k) // s + 1
+        if s == 1 and k in (3, 5) and c % 16 == 0 and ho >= 14 and wo >= 14 and (k == 3 or c <= 512):
+            return "dw_tc_i8_kernel"
     return {"dw": "dw_nhwc_kernel", "pw": "pw_tc_kernel", "dwpw": "dwpw_tc_kernel", "pwdw_r": "pwdw_tc_kernel",
             "pwpw": "pwpw_tc_kernel"}[op]
 
@@ -369,8 +377,10 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--batch", type=int, default=256, help="images per GPU")
     ap.add_argument("--mode", default="b200", choices=["b200", "paper"])
-    ap.add_argument("--plan", default="measured", choices=["measured", "model"],
-                    help="measured: refine the planner's choice with timed candidates (autotune.refine)")
+    ap.add_argument("--plan", default="measured", choices=["measured", "model", "all-dwpw"],
+                    help="measured: refine the planner's choice with timed candidates (autotune.refine); "
+                         "all-dwpw: every DW layer fused with its PW consumer (configs[1]'s 'FCM DWPW on "
+                         "every block'), whether or not it is faster")
     ap.add_argument("--plan-out", default="", help="write the executed plan (JSON) here")
     ap.add_argument("--ref-images", type=int, default=1, help="reference arm: images per step")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -412,6 +422,27 @@ def main():
             plan = refine(args.net, args.dtype, args.batch, device=dev)
             plan_verify = verify_against_lbl(args.net, args.dtype, plan, device=dev)
         plan = replicas.broadcast_plan(plan, ws)
+    elif args.plan == "all-dwpw":
+        plan = fcm.plan(model_json(args.net, args.dtype, args.batch, args.mode))
+        cands = plan["candidates"]
+        lbl = {c["layers"][0]: c for c in cands["lbl"]}
+        dwpw = {c["layers"][0]: c for c in cands["fcm"] if c["op"] == "dwpw"}
+        order = [c["layers"][0] for c in cands["lbl"]]
+        ents, i = [], 0
+        while i < len(order):
+            if order[i] in dwpw and i + 1 < len(order) and dwpw[order[i]]["layers"][1] == order[i + 1]:
+                ents.append(dwpw[order[i]])
+                i += 2
+            else:
+                ents.append(lbl[order[i]])
+                i += 1
+        plan = dict(plan, entries=ents, mode="all-dwpw",
+                    totals=dict(plan["totals"], fused_pairs=sum(len(e["layers"]) == 2 for e in ents),
+                                dram_bytes=sum(e["dram_bytes"] for e in ents)))
+        plan.pop("candidates", None)
+        if rank == 0:
+            from paper_2404_19331_b200.autotune import verify_against_lbl
+            plan_verify = verify_against_lbl(args.net, args.dtype, plan, device=dev)
     else:
         plan = fcm.plan(model_json(args.net, args.dtype, args.batch, args.mode))
     if args.plan_out and rank == 0:
@@ -528,7 +559,7 @@ def main():
     dw_mac_s = 148 * 128 * sm_hz
     tc_mac_s = float(pk.get("bf16_tflops", 1598.4)) * 1e12 / 2 * {"s8": 2.0, "f32": 0.5}.get(args.dtype, 1.0)
     for info, us, es in zip(netw.step_info, times_us, entry_stats):
-        k = kernel_family(info["op"])
+        k = kernel_family(info["op"], args.dtype, netw.layers[info["layers"][0]])
         f = fam.setdefault(k, {"us": 0.0, "bytes": 0, "n": 0, "bind_us": 0.0, "t": {"hbm": 0.0, "dw_alu": 0.0, "pw_tc": 0.0}})
         f["us"] += us
         f["bytes"] += info["dram_bytes"]

@@ -327,8 +327,20 @@ __global__ void pack_pw_kernel(const TT* __restrict__ w, TT* __restrict__ p, int
 }
 
 // ------------------------------------------------------------------------------- launchers
+static bool dw_tc_i8_enabled() {  // FCM_DW_I8_TC=0: the CUDA-core int8 DW (development comparison)
+  static const bool on = [] { const char* e = getenv("FCM_DW_I8_TC"); return !e || atoi(e) != 0; }();
+  return on;
+}
+
 template <int DT, int K, int S>
 static int launch_dw_t(const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  // int8, stride 1, k in {3, 5}, 16-byte pixel pitch, maps that fill its 16 x 8 output tiles: the
+  // tensor-core DW (tc.cu dw_tc_i8_kernel). Measured on B200 (EfficientNet-B0 / MobileNetV1 int8):
+  // 1.2-1.4x faster than this kernel on 112^2..14^2 maps, slower on 7^2 maps (38 % of the tile's
+  // rows live) and for 5x5 with C > 512 (one CTA per SM, the 25-tap MMA chain per tile)
+  if constexpr (DT == FCM_S8 && S == 1 && (K == 3 || K == 5))
+    if (g.C % 16 == 0 && g.Wo >= 14 && g.Ho >= 14 && (K == 3 || g.C <= 512) && dw_tc_i8_enabled())
+      return launch_dw_tc_i8(x, wdw, ep, y, g, st);
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   const int th = g.th, tw = g.tw;

@@ -55,6 +55,7 @@ int launch_pwdw_simt(int dt, const void* x, const void* wp, const Epi& ep, const
 int launch_pwpw_tc(int dt, const void* x, const void* w1, const Epi& ep1, const void* w2, const Epi& ep2, void* y,
                    int M, int K1, int Cmid, int N, cudaStream_t st);
 int launch_pack_pw(int dt, int cin, int cout, const void* w, void* packed, cudaStream_t st);
+int launch_dw_tc_i8(const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
 int launch_dw_nchw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
 
 int check_launch(const char* what);

@@ -1967,4 +1967,252 @@ int launch_pwpw_tc(int dt, const void* x, const void* w1, const Epi& ep1, const 
   return set_error(FCM_E_UNSUPPORTED, "pwpw tensor-core path: dtype");
 }
 
+
+// =====================================================================================
+// LBL int8 DW on the tensor cores (stride 1, k in {3, 5}). A depthwise tap is a matrix product
+// with a DIAGONAL weight block: for output pixels m (rows) and channels c of a 32-channel group,
+//   O[m, c] += X[m shifted by the tap, c] * w[tap, c]  =  (A_tap . diag(w_tap))[m, c]
+// with A_tap = the staged X halo tile viewed from the tap's offset. The X tile is TMA-loaded in the
+// 128-byte-swizzled K-major layout (a pixel = one 128-byte row of 128 int8 channels); an output
+// tile of 16 rows x 8 columns is M = 128 MMA rows whose 8-row core-matrix groups are the output
+// rows, so the tap view is the same tile descriptor started (dy * tw_in + dx) rows further with
+// SBO = tw_in * 128 B (no data movement; verified: tools/microbench/dw_mma_rate.cu). One
+// tcgen05.mma kind::i8 (M 128, N 32, K 32) per tap and 32-channel group accumulates exact int32 in
+// TMEM; 4 epilogue warps requantise (int32 bias, fixed-point multiplier, zero point, clamp:
+// reading R1) and store 128-bit rows. 32 of the 1024 MACs per weight column are useful, but the
+// tensor pipe still retires ~85 useful int8 MACs/clk/SM (MMA floor ~48 cycles, measured) against
+// ~17 for the CUDA-core int8 DW, and it leaves the CUDA cores to the epilogue.
+// Persistent: CTA (i, chunk) keeps the chunk's diagonal weight blocks (k^2 x 4 KB) resident and
+// loops over spatial tiles; 2-stage X ring, 2 TMEM accumulators; warp 0 TMA, warp 1 MMA, warps
+// 2-9 epilogue (TMEM lane quadrant = warp % 4, two warps per quadrant: the requantisation is the
+// CUDA-core work per output and bounds the kernel).
+// =====================================================================================
+constexpr int kDwTcTh = 16, kDwTcTw = 8;  // output tile (M = 128)
+#ifndef FCM_I8TC_FAST
+#define FCM_I8TC_FAST 0
+#endif
+
+// K-major operand, rows of xb = 32 / 64 / 128 bytes with the matching swizzle, 8-row groups SBO apart
+__device__ __forceinline__ uint64_t desc_swz_sbo(uint32_t saddr, int xb, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(xb == 128 ? 2 : (xb == 64 ? 4 : 6)) << 61;
+  return d;
+}
+__device__ __forceinline__ uint64_t desc_ns(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;
+}
+
+// 16 int32 accumulators of consecutive channels -> 4 packed int8 words: bias, requantisation (the
+// mad.hi fast form when the shift is >= 33, else the 64-bit form; identical results), zero point,
+// clamp. Constants from the staged per-channel arrays (broadcast loads: every lane reads the same
+// channel).
+__device__ __forceinline__ void epi16_i8_fast(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
+                                              uint32_t (&out)[4]) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint4 bq = lds128(cs.base + 4 * (n_base + 4 * w));
+    const uint4 mq = lds128(cs.base + 4 * (cs.ncap + n_base + 4 * w));
+    const uint4 sh = lds128(cs.base + 4 * (2 * cs.ncap + n_base + 4 * w));
+    const int32_t b4[4] = {(int32_t)bq.x, (int32_t)bq.y, (int32_t)bq.z, (int32_t)bq.w};
+    const int32_t m4[4] = {(int32_t)mq.x, (int32_t)mq.y, (int32_t)mq.z, (int32_t)mq.w};
+    const int32_t s4[4] = {(int32_t)sh.x, (int32_t)sh.y, (int32_t)sh.z, (int32_t)sh.w};
+    uint32_t word = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int32_t q = rq_apply(static_cast<int32_t>(r[4 * w + i]) + b4[i], make_rq(m4[i], s4[i]));
+      word |= (static_cast<uint32_t>(min(max(q + e.zp_out, e.qmin), e.qmax)) & 0xFFu) << (8 * i);
+    }
+    out[w] = word;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(320, K == 3 ? 2 : 1)  // 2 CTAs per SM for 3x3 (smem, TMEM, registers)
+    dw_tc_i8_kernel(const __grid_constant__ CUtensorMap tmx, const int8_t* __restrict__ wdw, Epi ep,
+                    int8_t* __restrict__ y, int N, int C, int Ho, int Wo, int pt, int pl, int tiles_x, int tiles_y,
+                    FDiv ftx, FDiv fty, int xb) {
+  pdl_launch();
+  constexpr int TH = kDwTcTh, TW = kDwTcTw;
+  constexpr int THI = TH + K - 1, TWI = TW + K - 1;
+  // X rows of xb bytes: 128-channel chunks, or the pixel's own 32 / 64 bytes when C is narrower
+  // (the matching 32 / 64 / 128-byte swizzle on both the TMA box and the MMA descriptor)
+  const int XB = (THI * TWI * xb + 1023) & ~1023;  // one X stage
+  constexpr int BB = K * K * 4 * 1024;                   // diagonal weight blocks of the chunk
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* xs = smem;              // 2 x XB
+  uint8_t* bs = xs + 2 * XB;       // BB
+  uint8_t* cst = bs + BB;          // int8 epilogue constants of the chunk (128 channels)
+  uint64_t* full = reinterpret_cast<uint64_t*>(cst + consts_bytes<FCM_S8>(128));
+  uint64_t* empty = full + 2;
+  uint64_t* tfull = empty + 2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cbase = blockIdx.y * 128;
+  const int cval = min(128, C - cbase);
+  const int ng = (cval + 31) >> 5;  // 32-channel groups with weights (MMAs past them are skipped)
+  // chunk constants and diagonal B blocks (weights are not produced by the previous kernel)
+  Epi e2 = ep;
+  if (e2.bias_q) e2.bias_q += cbase;
+  e2.mult_q += cbase;
+  e2.shift_q += cbase;
+  const EpiS cs = stage_consts<FCM_S8>(e2, cval, 128, cst);
+  for (int i = threadIdx.x; i < BB / 16; i += blockDim.x) sts128(smem_u32(bs) + 16 * i, 0, 0, 0, 0);
+  __syncthreads();
+  // B(tap, g)[n][k] = (n == k) ? w[tap][cbase + 32 g + n] : 0, K-major no-swizzle: 8-row x 16-byte
+  // core matrices, LBO 128 (next 16 K bytes), SBO 256 (next 8 rows); 1 KB per (tap, group)
+  for (int i = threadIdx.x; i < K * K * 128; i += blockDim.x) {
+    const int t = i >> 7, c = i & 127, g = c >> 5, n = c & 31;
+    const int8_t v = c < cval ? __ldg(wdw + (size_t)t * C + cbase + c) : int8_t(0);
+    const uint32_t off = (t * 4 + g) * 1024 + (n >> 3) * 256 + (n >> 4) * 128 + (n & 7) * 16 + (n & 15);
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(smem_u32(bs) + off), "h"((unsigned short)(uint8_t)v) : "memory");
+  }
+  fence_proxy_async_smem();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmx);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+      mbar_init(tfull + i, 1);
+      mbar_init(tempty + i, 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_rt(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tbase = *tslot;
+  const int total = N * tiles_y * tiles_x;
+  auto decode = [&](int t, int& n, int& ty, int& tx) {
+    const int q = fdiv(t, ftx);
+    tx = t - q * tiles_x;
+    n = fdiv(q, fty);
+    ty = q - n * tiles_y;
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      Ring rs(2);
+      for (int t = blockIdx.x; t < total; t += gridDim.x, rs.next()) {
+        int n, ty, tx;
+        decode(t, n, ty, tx);
+        mbar_wait_sleep<128>(empty + rs.i, rs.ph ^ 1);
+        mbar_arrive_expect_tx(full + rs.i, THI * TWI * xb);
+        tma_load_4d(xs + rs.i * XB, &tmx, full + rs.i, cbase, tx * TW - pl, ty * TH - pt, n);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(TcKind<FCM_S8>::cf, TcKind<FCM_S8>::ab, 128, 32);
+      const uint64_t b0 = desc_ns(smem_u32(bs), 128, 256);
+      Ring rs(2), ra(2);
+      for (int t = blockIdx.x; t < total; t += gridDim.x, rs.next(), ra.next()) {
+        mbar_wait_sleep<128>(tempty + ra.i, ra.ph ^ 1);
+        mbar_wait_sleep<64>(full + rs.i, rs.ph);
+        tc_fence_after();
+        const uint64_t a0 = desc_swz_sbo(smem_u32(xs + rs.i * XB), xb, TWI * xb);
+        const uint32_t d = tbase + ra.i * 128;
+        const uint32_t xr = (uint32_t)xb >> 4;  // one pixel row, in 16-byte descriptor units
+#pragma unroll
+        for (int tap = 0; tap < K * K; ++tap)
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (g < ng)
+              mma_ss<MmaKind::I8>(d + g * 32, a0 + (uint64_t)(((tap / K) * TWI + tap % K) * xr + g * 2),
+                                  b0 + (uint64_t)(((tap * 4 + g) * 1024) >> 4), idesc, tap != 0);
+        mma_commit(empty + rs.i);
+        mma_commit(tfull + ra.i);
+      }
+    }
+  } else {
+    // epilogue (8 warps): lane = one output pixel (row m = 32 q + lane of the 16 x 8 tile); the two
+    // warps of a TMEM lane quadrant take 64 channels each
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int m = q * 32 + lane;
+    const int r = m >> 3, c = m & 7;
+    Ring ra(2);
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ra.next()) {
+      int n, ty, tx;
+      decode(t, n, ty, tx);
+      const int yo = ty * TH + r, xo = tx * TW + c;
+      const bool ok = yo < Ho && xo < Wo;
+      int8_t* dst = y + (((size_t)n * Ho + yo) * Wo + xo) * C + cbase;
+      group_wait_sleep(tfull + ra.i, ra.ph, warp == 2, 1, 256);
+      tc_fence_after();
+      const uint32_t tq = tbase + ra.i * 128 + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c32 = half * 64; c32 < half * 64 + 64; c32 += 32) {
+        if (c32 >= cval) break;
+        uint32_t acc[32];
+        tmem_ld32(tq + c32, acc);
+        tmem_ld_wait();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+#if FCM_I8TC_FAST
+          uint32_t o[4];
+          epi16_i8_fast(&acc[16 * hh], cs, ep, c32 + 16 * hh, o);
+#else
+          uint32_t o[8];
+          epi16<FCM_S8>(&acc[16 * hh], cs, ep, c32 + 16 * hh, o);
+#endif
+          if (ok && c32 + 16 * hh < cval) stg128(dst + c32 + 16 * hh, o[0], o[1], o[2], o[3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + ra.i);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_rt(tbase, 256);
+  }
+}
+
+template <int K>
+static int launch_dw_tc_i8_t(const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  constexpr int THI = kDwTcTh + K - 1, TWI = kDwTcTw + K - 1;
+  const int xb = g.C <= 32 ? 32 : (g.C <= 64 ? 64 : 128);
+  CUtensorMap tm;
+  const uint64_t dims[4] = {(uint64_t)g.C, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N};
+  const uint64_t str[3] = {(uint64_t)g.C, (uint64_t)g.W * g.C, (uint64_t)g.H * g.W * g.C};
+  const uint32_t box[4] = {(uint32_t)xb, (uint32_t)TWI, (uint32_t)THI, 1u};
+  const CUtensorMapSwizzle sw = xb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                          : (xb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!encode_tmap(&tm, tmap_dtype(FCM_S8), 4, x, dims, str, box, sw))
+    return set_error(FCM_E_CUDA, "tensor map (int8 tensor-core DW X) failed");
+  const int tiles_x = (g.Wo + kDwTcTw - 1) / kDwTcTw, tiles_y = (g.Ho + kDwTcTh - 1) / kDwTcTh;
+  const int spatial = g.N * tiles_x * tiles_y, nchunk = (g.C + 127) / 128;
+  const int xst = (THI * TWI * xb + 1023) & ~1023;
+  const size_t smem = 1024 + 2 * (size_t)xst + K * K * 4 * 1024 + consts_bytes<FCM_S8>(128) + 128;
+  if (smem > (size_t)device_props().smem_optin) return set_error(FCM_E_INFEASIBLE, "int8 tensor-core DW: smem");
+  const int per_sm = smem * 2 <= (size_t)device_props().smem_optin ? 2 : 1;  // TMEM: 256 columns per CTA
+  const int gx = std::max(1, std::min(spatial, (device_props().sms * per_sm + nchunk - 1) / nchunk));
+  auto kern = dw_tc_i8_kernel<K>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_k(kern, dim3(gx, nchunk), dim3(320), smem, st, tm, static_cast<const int8_t*>(wdw), ep,
+           static_cast<int8_t*>(y), g.N, g.C, g.Ho, g.Wo, g.pt, g.pl, tiles_x, tiles_y, make_fdiv(tiles_x),
+           make_fdiv(tiles_y), xb);
+  return check_launch("dw_tc_i8_kernel");
+}
+
+int launch_dw_tc_i8(const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st) {
+  if (g.s != 1 || g.C % 16 != 0) return set_error(FCM_E_UNSUPPORTED, "int8 tensor-core DW: stride 1, C % 16 == 0");
+  if (g.k == 3) return launch_dw_tc_i8_t<3>(x, wdw, ep, y, g, st);
+  if (g.k == 5) return launch_dw_tc_i8_t<5>(x, wdw, ep, y, g, st);
+  return set_error(FCM_E_UNSUPPORTED, "int8 tensor-core DW: k in {3, 5}");
+}
+
 }  // namespace fcm

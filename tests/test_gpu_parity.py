@@ -34,6 +34,29 @@ def test_dw(fmt, k, s):
     Case("dw", fmt, 2, 23, 29, c, k=k, s=s).check()
 
 
+# int8 stride-1 3x3 / 5x5 DW on maps >= 14 x 14 runs on the tensor cores (diagonal weight blocks,
+# row-shifted swizzled views of the X tile; tc.cu dw_tc_i8_kernel): partial 128-channel chunks and
+# 32-channel groups, 32 / 64 / 128-byte X rows, ragged 16 x 8 tiles, asymmetric pads; bit-exact vs
+# the oracle. (Smaller maps and 5x5 with C > 512 take the CUDA-core kernel: last two cases.)
+@pytest.mark.parametrize("k", [3, 5])
+@pytest.mark.parametrize("n,h,w,c,pads", [
+    (1, 17, 19, 16, None),           # one 16-channel group (32-byte rows), ragged tile in both directions
+    (2, 23, 29, 144, None),          # 128 + 16 channels (partial chunk)
+    (1, 15, 15, 48, (0, 2, 1, 0)),   # asymmetric pads, 64-byte rows, partial 32-channel group
+    (3, 14, 14, 256, None),          # MobileNetV2-like map, two chunks
+    (1, 30, 14, 96, None),           # 64 + 32 channels in one 128-byte chunk
+    (1, 1, 3, 32, None),             # tiny map (CUDA-core kernel)
+    (1, 14, 14, 528, None),          # 5x5 with C > 512 on the CUDA-core kernel, 3x3 on the tensor cores
+])
+def test_dw_int8_tensor_core(k, n, h, w, c, pads):
+    Case("dw", "s8", n, h, w, c, k=k, s=1, pads=pads).check()
+
+
+def test_dw_int8_tensor_core_steady_state():
+    # >= 3 tiles per CTA at 2 CTAs per SM: 148 * 2 * 3 spatial tiles of 16 x 8 per 128-channel chunk
+    Case("dw", "s8", 24, 56, 56, 128, k=3, s=1).check()
+
+
 def test_dw_asymmetric_pads_and_tiny():
     Case("dw", "bf16", 1, 1, 1, 16, k=3, s=1).check()
     Case("dw", "bf16", 2, 12, 12, 24, k=3, s=2, pads=(0, 0, 1, 1)).check()
