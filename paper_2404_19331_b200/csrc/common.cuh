@@ -186,6 +186,7 @@ __device__ __forceinline__ void load_dw_weights(DwW<DT, K>& W, const typename Tr
 struct EpiS {
   uint32_t base;  // shared-space byte address
   int ncap;
+  int fast;       // int8: every staged shift >= 33 (the one-mad.hi requantisation applies to all columns)
   __device__ __forceinline__ float sc(int n) const { return __uint_as_float(lds32(base + 4 * n)); }
   __device__ __forceinline__ float bi(int n) const { return __uint_as_float(lds32(base + 4 * (ncap + n))); }
   __device__ __forceinline__ int32_t bq(int n) const { return (int32_t)lds32(base + 4 * n); }
@@ -199,6 +200,7 @@ template <int DT>
 __device__ __forceinline__ EpiS stage_consts(const Epi& e, int N, int ncap, uint8_t* area) {
   const uint32_t base = smem_u32(area);
   const int nt = blockDim.x;
+  bool fast = true;
   for (int i0 = threadIdx.x; i0 < ncap; i0 += 4 * nt) {
     uint32_t a[4], b[4], c[4];
 #pragma unroll
@@ -209,6 +211,7 @@ __device__ __forceinline__ EpiS stage_consts(const Epi& e, int N, int ncap, uint
         a[u] = (v && e.bias_q) ? (uint32_t)__ldg(e.bias_q + i) : 0u;
         b[u] = v ? (uint32_t)__ldg(e.mult_q + i) : 0u;
         c[u] = v ? (uint32_t)__ldg(e.shift_q + i) : 1u;
+        fast = fast && (!v || (int32_t)c[u] >= 33);
       } else {
         a[u] = __float_as_uint(v ? (e.scale ? __ldg(e.scale + i) : 1.f) : 0.f);
         b[u] = __float_as_uint((v && e.bias) ? __ldg(e.bias + i) : 0.f);
@@ -224,7 +227,9 @@ __device__ __forceinline__ EpiS stage_consts(const Epi& e, int N, int ncap, uint
       }
     }
   }
-  return EpiS{base, ncap};
+  // block-wide: every caller stages its constants with all threads at kernel entry
+  const int f = DT == FCM_S8 ? __syncthreads_and(fast) : 0;
+  return EpiS{base, ncap, f};
 }
 template <int DT> constexpr int consts_bytes(int ncap) { return (DT == FCM_S8 ? 12 : 8) * ncap; }
 

@@ -64,6 +64,27 @@ template <int DT, bool RES = false, bool SMOOTH = true>
 __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const Epi& e, int n_base,
                                       uint32_t (&out)[8], uint4 ra = uint4{}, uint4 rb = uint4{}) {
   if constexpr (DT == FCM_S8) {
+    if (cs.fast) {  // CTA-uniform: all shifts >= 33 -> one mad.hi + shift per value (identical results)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint4 bq = lds128(cs.base + 4 * (n_base + 4 * w));
+        const uint4 mq = lds128(cs.base + 4 * (cs.ncap + n_base + 4 * w));
+        const uint4 sh = lds128(cs.base + 4 * (2 * cs.ncap + n_base + 4 * w));
+        const int32_t b4[4] = {(int32_t)bq.x, (int32_t)bq.y, (int32_t)bq.z, (int32_t)bq.w};
+        const int32_t m4[4] = {(int32_t)mq.x, (int32_t)mq.y, (int32_t)mq.z, (int32_t)mq.w};
+        const int32_t s4[4] = {(int32_t)sh.x, (int32_t)sh.y, (int32_t)sh.z, (int32_t)sh.w};
+        uint32_t word = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int32_t h;
+          asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(h) : "r"(static_cast<int32_t>(r[4 * w + i]) + b4[i]), "r"(m4[i]),
+              "r"(1 << (s4[i] - 33)));
+          word |= (static_cast<uint32_t>(min(max((h >> (s4[i] - 32)) + e.zp_out, e.qmin), e.qmax)) & 0xFFu) << (8 * i);
+        }
+        out[w] = word;
+      }
+      return;
+    }
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const uint4 bq = lds128(cs.base + 4 * (n_base + 4 * w));
