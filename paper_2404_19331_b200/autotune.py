@@ -73,7 +73,15 @@ def dwpw_tile_alternatives(tile, ho, wo, k, s, cout, dtype, limit=10):
     # prefer tiles near the planner's pixel count (keeps the search short)
     px0 = tile["tile_n"] * tile["tile_h"] * tile["tile_w"]
     rest = sorted(uniq[1:], key=lambda t: abs(t["tile_n"] * t["tile_h"] * t["tile_w"] - px0))
-    return [uniq[0]] + rest[:limit - 1]
+    sel = [uniq[0]] + rest[:limit - 1]
+    # small maps (7^2, 14^2): a C_out split multiplies the CTAs (the DW stage is recomputed per
+    # split, cheap at these sizes) when the tiles alone leave SMs idle or a ragged last wave
+    if ho * wo <= 14 * 14 and cout >= 64:
+        for t in list(sel[:3]):
+            for ns in (2, 4):
+                if cout // ns >= 16 and t.get("n_split", 1) == 1:
+                    sel.append(dict(t, n_split=ns))
+    return sel
 
 
 def pwdw_tile_alternatives(tile, ho, wo, k, s, dtype, limit=10):
