@@ -122,11 +122,13 @@ typedef struct {
 } fcm_epilogue;
 
 /* Optional tile override (NULL = the library's default for the shape). Output-space tile
- * tile_h x tile_w pixels of tile_n images; n_split = number of C_out slices (DWPW) or the
- * intermediate-channel slice width td (PWDW_R, as c_chunk). 0 = default for that field.
- * DWPW tiles hold at most 256 pixels (two M=128 MMA row blocks) on the bf16/f16 3x3 path and
- * 128 otherwise; PWDW_R halo tiles at most 256 pixels. A tile whose staging does not fit shared
- * memory / TMEM returns FCM_E_INFEASIBLE. */
+ * tile_h x tile_w pixels of tile_n images; n_split = number of C_out slices (DWPW, and the
+ * tensor-core PW: its only tile field) or the intermediate-channel slice width td (PWDW_R, as
+ * c_chunk). 0 = default for that field. DWPW tiles hold at most 256 pixels (two M=128 MMA row
+ * blocks) on the bf16/f16 3x3 path and 128 otherwise; PWDW_R halo tiles at most 512 pixels for
+ * bf16/f16 (four row blocks), 256 for int8. The int8 stride-1 3x3 / 5x5 DW on maps >= 14 x 14
+ * runs on the tensor cores with a fixed 16 x 8 output tile (the tile is ignored there). A tile
+ * whose staging does not fit shared memory / TMEM returns FCM_E_INFEASIBLE. */
 typedef struct {
   int32_t tile_h, tile_w, tile_n, c_chunk, n_split;
 } fcm_tile;

@@ -175,6 +175,10 @@ def refine(net: str, dtype: str, batch: int, device="cuda", reps=10, verbose=Fal
             ho = (d["h"] + 2 * (kk // 2) - kk) // ss + 1
             wo = (d["w"] + 2 * (kk // 2) - kk) // ss + 1
             tiles = dwpw_tile_alternatives(c["tile"], ho, wo, kk, ss, probe.layers[lids[1]]["c_out"], dtype)
+        elif tile_search and c["op"] == "pw" and c.get("tile") and dtype in ("bf16", "f16", "s8"):
+            cout = probe.layers[lids[0]]["c_out"]
+            tiles = [c["tile"]] + [dict(c["tile"], n_split=ns) for ns in (1, 2, 3, 4, 6, 8)
+                                   if ns != c["tile"].get("n_split") and -(-cout // ns) >= 16 and -(-cout // ns) <= 256]
         elif tile_search and c["op"] == "pwdw_r" and c.get("tile") and dtype in ("bf16", "f16", "s8"):
             d = probe.layers[lids[1]]
             kk, ss = d["k"], d["stride"]

@@ -246,7 +246,6 @@ int fcm_dw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const
 
 int fcm_pw(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep, fcm_tensor* y, const fcm_tile* tile,
            void* stream) {
-  (void)tile;
   FCM_TRY(check_tensor(x, "x", false));
   FCM_TRY(check_tensor(y, "y", false));
   if (!w_pw_packed) return set_error(FCM_E_INVAL, "w_pw is NULL");
@@ -259,7 +258,9 @@ int fcm_pw(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y))
     return launch_pw_simt(x->dtype, x->data, w_pw_packed, to_epi(ep), y->data, M, x->c, y->c, st);
-  return launch_pw_tc(x->dtype, x->data, w_pw_packed, to_epi(ep), y->data, M, x->c, y->c, st);
+  // tile: only n_split (the number of C_out slices) applies to the tensor-core PW
+  return launch_pw_tc(x->dtype, x->data, w_pw_packed, to_epi(ep), y->data, M, x->c, y->c,
+                      tile && tile->n_split > 0 ? tile->n_split : 0, st);
 }
 
 int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const fcm_epilogue* ep_dw,

@@ -41,7 +41,8 @@ struct Geo {
 
 // launchers (return FCM_OK or an FCM_E_* code; all validation already done by the API layer)
 int launch_dw(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
-int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st);
+int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, int nsplit,
+                 cudaStream_t st);  // nsplit <= 0: default C_out split
 int launch_pw_simt(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st);
 int launch_dw_simt(int dt, const void* x, const void* wdw, const Epi& ep, void* y, const Geo& g, cudaStream_t st);
 int launch_dwpw_tc(int dt, const void* x, const void* wdw, const Epi& ed, const void* wp, const Epi& ep, void* y,

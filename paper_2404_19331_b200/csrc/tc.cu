@@ -1395,11 +1395,12 @@ static bool out_tmap_2d(CUtensorMap* m, int dt, void* y, int M, int N) {
 }
 
 template <int DT>
-static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st) {
+static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, int nsplit_req,
+                       cudaStream_t st) {
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   int nbn = 0;
-  const int BN = pick_bn<DT>(N, 0, nbn);
+  const int BN = pick_bn<DT>(N, nsplit_req, nbn);
   CUtensorMap ta, tb, ty;
   {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
@@ -1458,11 +1459,12 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   return rc;
 }
 
-int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, cudaStream_t st) {
+int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, int nsplit,
+                 cudaStream_t st) {
   switch (dt) {
-    case FCM_BF16: return launch_pw_t<FCM_BF16>(x, wp, ep, y, M, K, N, st);
-    case FCM_F16: return launch_pw_t<FCM_F16>(x, wp, ep, y, M, K, N, st);
-    case FCM_S8: return launch_pw_t<FCM_S8>(x, wp, ep, y, M, K, N, st);
+    case FCM_BF16: return launch_pw_t<FCM_BF16>(x, wp, ep, y, M, K, N, nsplit, st);
+    case FCM_F16: return launch_pw_t<FCM_F16>(x, wp, ep, y, M, K, N, nsplit, st);
+    case FCM_S8: return launch_pw_t<FCM_S8>(x, wp, ep, y, M, K, N, nsplit, st);
   }
   return set_error(FCM_E_UNSUPPORTED, "pw tensor-core path: dtype");
 }

@@ -166,7 +166,7 @@ class Network:
         if op == "pw":
             w, ep = self.params[lids[0]]
             ep = withres(ep)
-            return lambda: fcm.pw(src, w, ep, out=out)
+            return lambda: fcm.pw(src, w, ep, out=out, tile=tile)
         if op == "dwpw":
             l = self.layers[lids[0]]
             (wd, ed), (wp, ep) = self.params[lids[0]], self.params[lids[1]]
