@@ -158,7 +158,7 @@ class Case:
         elif self.op == "dw":
             y = fcm.dw(x, wdw, self.s, self.pads, ed, tile=self.tile)
         elif self.op == "pw":
-            y = fcm.pw(x, wpk, ep)
+            y = fcm.pw(x, wpk, ep, tile=self.tile)
         elif self.op == "dwpw":
             y = fcm.dwpw(x, wdw, self.s, self.pads, ed, wpk, ep, tile=self.tile)
         else:

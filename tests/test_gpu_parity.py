@@ -166,6 +166,17 @@ def test_pwdw_r_wide_halo_narrow_x(fmt, c_in, s, h, w, tile):
     Case("pwdw", fmt, 2, h, w, c_in, 96, k=3, s=s, tile=tile).check()
 
 
+@pytest.mark.parametrize("fmt", ["bf16", "s8"])
+@pytest.mark.parametrize("n_split", [1, 3, 6])
+def test_pw_explicit_cout_split(fmt, n_split):
+    """The tensor-core PW's C_out split (tile n_split, searched by the measured plan) changes the
+    tiling, never the values: oracle parity and bitwise equality with the default split."""
+    c = Case("pw", fmt, 2, 13, 11, 48, 384, tile=dict(n_split=n_split))
+    c.check()
+    d = Case("pw", fmt, 2, 13, 11, 48, 384)
+    assert np.array_equal(c.gpu(), d.gpu())
+
+
 def test_pwdw_r_wide_halo_tiling_invariance_bitwise():
     outs = []
     for tile in [dict(tile_h=4, tile_w=4), dict(tile_h=7, tile_w=14), dict(tile_h=8, tile_w=14), dict(tile_h=15, tile_w=3)]:

@@ -26,6 +26,14 @@ for args, kw in [(("dw", "bf16", 1, 9, 11, 64), {}), (("dw", "s8", 1, 9, 7, 32),
                  # (pixel pitch not a multiple of 16 B) incl. k = 7
                  (("dwpw", "s8", 1, 9, 11, 160, 64), {}), (("dwpw", "s8", 1, 12, 13, 128, 32), {"s": 2}),
                  (("dw", "s8", 1, 7, 9, 728), {}), (("dw", "bf16", 1, 9, 8, 36), {"k": 7, "s": 2}),
-                 (("dw", "s8", 1, 9, 9, 40), {"k": 7})]:
+                 (("dw", "s8", 1, 9, 9, 40), {"k": 7}),
+                 # round 2: int8 tensor-core DW (128-byte chunk + partial group, 32-byte rows, 5x5),
+                 # PWDW_R with 32/64-byte X rows, 4-row-block halos, lane groups, resident slices;
+                 # DWPW 4-column items with a residual; PW with an explicit C_out split
+                 (("dw", "s8", 1, 17, 19, 144), {}), (("dw", "s8", 1, 15, 16, 16), {"k": 5}),
+                 (("pwdw", "bf16", 1, 30, 29, 16, 96), {"s": 2, "tile": dict(tile_h=7, tile_w=14)}),
+                 (("pwdw", "f16", 1, 23, 26, 72, 96), {"tile": dict(tile_h=16, tile_w=16)}),
+                 (("dwpw", "bf16", 2, 14, 14, 96, 32), {"residual": True, "tile": dict(tile_h=14, tile_w=14)}),
+                 (("pw", "bf16", 2, 13, 11, 24, 144), {"tile": dict(n_split=3)})]:
     Case(*args, **kw).check()
     print("ok", args, kw, flush=True)
