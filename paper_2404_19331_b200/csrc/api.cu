@@ -256,7 +256,10 @@ int fcm_pw(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep,
   if (overlaps(x, y)) return set_error(FCM_E_INVAL, "pw: x and y overlap");
   const int M = x->n * x->h * x->w;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y))
+  // fp32: 3xTF32 on the tensor cores (FCM_PW_F32_TC=0: the FFMA kernel)
+  static const bool f32_tc = [] { const char* e = getenv("FCM_PW_F32_TC"); return !e || atoi(e) != 0; }();
+  const bool f32_simt = x->dtype == FCM_F32 && !f32_tc;
+  if (f32_simt || !pitch_ok(x) || !pitch_ok(y))
     return launch_pw_simt(x->dtype, x->data, w_pw_packed, to_epi(ep), y->data, M, x->c, y->c, st);
   // tile: only n_split (the number of C_out slices) applies to the tensor-core PW
   return launch_pw_tc(x->dtype, x->data, w_pw_packed, to_epi(ep), y->data, M, x->c, y->c,

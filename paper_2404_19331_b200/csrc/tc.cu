@@ -25,6 +25,9 @@ template <int DT> struct TcKind;
 template <> struct TcKind<FCM_BF16> { static constexpr MmaKind kind = MmaKind::F16; static constexpr uint32_t cf = 1, ab = 1; };
 template <> struct TcKind<FCM_F16> { static constexpr MmaKind kind = MmaKind::F16; static constexpr uint32_t cf = 1, ab = 0; };
 template <> struct TcKind<FCM_S8> { static constexpr MmaKind kind = MmaKind::I8; static constexpr uint32_t cf = 2, ab = 1; };
+// fp32 PW: kind::tf32 with the 3xTF32 split (x = x_hi + x_lo, w = w_hi + w_lo; x_hi.w_hi + x_hi.w_lo
+// + x_lo.w_hi, the dropped x_lo.w_lo term is ~2^-22 relative: reading R10b's 1e-5 is met)
+template <> struct TcKind<FCM_F32> { static constexpr MmaKind kind = MmaKind::TF32; static constexpr uint32_t cf = 1, ab = 2; };
 // K elements per tcgen05.mma instruction (32 bytes of each operand row)
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -262,6 +265,31 @@ __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0
     for (int c32 = 0; c32 < CPC; c32 += 32) {
       const int c0 = cc * CPC + c32;
       if (c0 >= BN) break;
+      if constexpr (ES == 4) {
+        // fp32 output (3xTF32 PW): v = act(acc * scale + bias) (+ residual), 32 columns = one
+        // 128-byte chunk
+        uint32_t r[32];
+        tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + c0, r);
+        const float* rp = e.residual ? static_cast<const float*>(e.residual) + (size_t)grow * N + n0 + c0 : nullptr;
+        tmem_ld_wait();
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint4 sc = lds128(cs.base + 4 * (n0 + c0 + 4 * v));
+          const uint4 bi = lds128(cs.base + 4 * (cs.ncap + n0 + c0 + 4 * v));
+          float4 rs = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (rp && grow < M && n0 + c0 + 4 * v < N) {
+            const uint4 w = ldg_nc128(rp + 4 * v);
+            rs = make_float4(__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z), __uint_as_float(w.w));
+          }
+          const float* a = reinterpret_cast<const float*>(&r[4 * v]);
+          sts128(smem_u32(buf) + sw128_vec(lane, v),
+                 __float_as_uint(act_f(fmaf(a[0], __uint_as_float(sc.x), __uint_as_float(bi.x)), e.act) + rs.x),
+                 __float_as_uint(act_f(fmaf(a[1], __uint_as_float(sc.y), __uint_as_float(bi.y)), e.act) + rs.y),
+                 __float_as_uint(act_f(fmaf(a[2], __uint_as_float(sc.z), __uint_as_float(bi.z)), e.act) + rs.z),
+                 __float_as_uint(act_f(fmaf(a[3], __uint_as_float(sc.w), __uint_as_float(bi.w)), e.act) + rs.w));
+        }
+        continue;
+      }
       if (ES == 2 && (hasres || e.act > FCM_ACT_RELU6)) {
         // SiLU / GELU / residual: 16 columns per TMEM load, the residual words
         // issued before it (register budget 18 warps x 96; the 16 epilogue warps hide the latency)
@@ -316,7 +344,7 @@ __device__ __forceinline__ void epilogue_tile_warp(uint32_t tacc, int BN, int n0
 // rest idle while its TMEM round trips serialise.
 // =====================================================================================
 template <int DT>
-__global__ void __launch_bounds__(576, 1)
+__global__ void __launch_bounds__(DT == FCM_F32 ? 640 : 576, 1)
     pw_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                  const __grid_constant__ CUtensorMap tmy, Epi ep, int M, int N, int K, int BN, int nbn, FDiv fnbn,
                  int stages, int ng, int nbuf, uint32_t tmem_cols, int ncap, int resB, unsigned long long* trace,
@@ -328,17 +356,23 @@ __global__ void __launch_bounds__(576, 1)
   constexpr int KSTEP = 32 / Tr<DT>::ES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
+  // kSplit (fp32, 3xTF32): every stage also holds x_lo and w_lo; two converter warps (18, 19) split
+  // the landed tiles in place (hi = the value with its low 13 mantissa bits cleared, exact in tf32)
+  constexpr bool kSplit = DT == FCM_F32;
+  constexpr int AST = kSplit ? 32768 : 16384;    // A stage: x (-> x_hi) [+ x_lo]
+  const int BST = BN * 128 * (kSplit ? 2 : 1);   // B stage: w (-> w_hi) [+ w_lo]
   uint8_t* stage = smem;                         // 16 warps x 4 KB output staging
   uint8_t* abuf = smem + 65536;
-  uint8_t* bbuf = abuf + stages * 16384;         // resB: all nk chunks of this CTA's B slice, else a ring
+  uint8_t* bbuf = abuf + stages * AST;           // resB: all nk chunks of this CTA's B slice, else a ring
   const int nk = (K + KC - 1) / KC;
-  uint8_t* cst = bbuf + (resB ? nk : stages) * BN * 128;
+  uint8_t* cst = bbuf + (resB ? nk * BN * 128 : stages * BST);
   uint64_t* full = reinterpret_cast<uint64_t*>(cst + consts_bytes<DT>(ncap));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 8;
   uint64_t* bfull = tempty + 8;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* cfull = bfull + 1;                   // kSplit: stage converted
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(cfull + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, N, ncap, cst);
   const int spg = 4 / ng;  // warps per TMEM lane quadrant in one group
@@ -349,6 +383,7 @@ __global__ void __launch_bounds__(576, 1)
     for (int s = 0; s < stages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
     for (int a = 0; a < nbuf * ng; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4 * spg); }
     mbar_init(bfull, 1);
+    for (int s = 0; s < stages && kSplit; ++s) mbar_init(cfull + s, 2);
     fence_barrier_init();
   }
   if (warp == 17) tmem_alloc_rt(tslot, tmem_cols);
@@ -387,8 +422,8 @@ __global__ void __launch_bounds__(576, 1)
           mbar_wait(empty + rs.i, rs.ph ^ 1);
           if (kc == 0) stamp(lt, 8);
           mbar_arrive_expect_tx(full + rs.i, 16384 + (resB ? 0 : BN * 128));
-          tma_load_2d(abuf + rs.i * 16384, &tma, full + rs.i, kc * KC, m0);
-          if (!resB) tma_load_2d(bbuf + rs.i * BN * 128, &tmb, full + rs.i, kc * KC, n0);
+          tma_load_2d(abuf + rs.i * AST, &tma, full + rs.i, kc * KC, m0);
+          if (!resB) tma_load_2d(bbuf + rs.i * BST, &tmb, full + rs.i, kc * KC, n0);
         }
       }
     }
@@ -407,18 +442,54 @@ __global__ void __launch_bounds__(576, 1)
         tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         for (int kc = 0; kc < nk; ++kc, rs.next()) {
-          mbar_wait(full + rs.i, rs.ph);
+          mbar_wait(kSplit ? cfull + rs.i : full + rs.i, rs.ph);
           if (kc == 0) stamp(local, 1);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(smem_u32(abuf + rs.i * 16384));
-          const uint64_t bd = smem_desc_sw128(smem_u32(bbuf + (resB ? kc : rs.i) * BN * 128));
+          const uint64_t ad = smem_desc_sw128(smem_u32(abuf + rs.i * AST));
+          const uint64_t bd = smem_desc_sw128(smem_u32(resB ? bbuf + kc * BN * 128 : bbuf + rs.i * BST));
           const int ksteps = min(4, (K - kc * KC + KSTEP - 1) / KSTEP);  // skip all-zero K steps
-          for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+          if constexpr (kSplit) {
+            const uint64_t adl = ad + (16384 >> 4), bdl = bd + ((BN * 128) >> 4);  // x_lo, w_lo
+            for (int k = 0; k < ksteps; ++k) {
+              mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+              mma_ss<KIND>(d, ad + 2 * k, bdl + 2 * k, idesc, 1);
+              mma_ss<KIND>(d, adl + 2 * k, bd + 2 * k, idesc, 1);
+            }
+          } else {
+            for (int k = 0; k < ksteps; ++k) mma_ss<KIND>(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+          }
           mma_commit(empty + rs.i);
         }
         mma_commit(tfull + acc);
         stamp(local, 2);
       }
+    }
+  } else if (warp >= 18) {
+    // kSplit converters: x -> (x_hi in place, x_lo), w -> (w_hi in place, w_lo) per landed stage
+    if constexpr (kSplit) {
+      const int ct = threadIdx.x - 18 * 32;
+      Ring rs(stages);
+      for (int t = blockIdx.x; t < total; t += gridDim.x)
+        for (int kc = 0; kc < nk; ++kc, rs.next()) {
+          mbar_wait(full + rs.i, rs.ph);
+          auto split = [&](uint32_t hi_base, uint32_t lo_base, int nvec) {
+            for (int v = ct; v < nvec; v += 64) {
+              const uint4 x = lds128(hi_base + 16 * v);
+              const uint4 h = make_uint4(x.x & 0xFFFFE000u, x.y & 0xFFFFE000u, x.z & 0xFFFFE000u, x.w & 0xFFFFE000u);
+              sts128(hi_base + 16 * v, h.x, h.y, h.z, h.w);
+              sts128(lo_base + 16 * v, __float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x)),
+                     __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y)),
+                     __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z)),
+                     __float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w)));
+            }
+          };
+          const uint32_t a = smem_u32(abuf + rs.i * AST), b = smem_u32(bbuf + rs.i * BST);
+          split(a, a + 16384, 1024);
+          split(b, b + BN * 128, BN * 8);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) mbar_arrive(cfull + rs.i);
+        }
     }
   } else {
     // epilogue warp: lane quadrant q = warp % 4, group g, slot hs within the group
@@ -1400,7 +1471,8 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   constexpr int ES = Tr<DT>::ES;
   constexpr int KC = 128 / ES;
   int nbn = 0;
-  const int BN = pick_bn<DT>(N, nsplit_req, nbn);
+  int BN = pick_bn<DT>(N, nsplit_req, nbn);
+  if (DT == FCM_F32 && BN > 128) BN = pick_bn<DT>(N, (N + 127) / 128, nbn);  // 3xTF32 stages hold x, x_lo, w, w_lo
   CUtensorMap ta, tb, ty;
   {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
@@ -1426,7 +1498,7 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   // resident B: the CTA keeps its whole C_out slice of the weights in smem (grid a multiple of nbn
   // so the slice is fixed) when that still leaves >= 4 A stages
   const int resgrid = (grid / nbn) * nbn;
-  const bool resB = resgrid > 0 && budget - nk * BN * 128 >= 4 * 16384 && resgrid >= grid * 15 / 16;
+  const bool resB = DT != FCM_F32 && resgrid > 0 && budget - nk * BN * 128 >= 4 * 16384 && resgrid >= grid * 15 / 16;
   int stages;
   size_t smem;
   if (resB) {
@@ -1434,7 +1506,7 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
     stages = std::min(std::max(2 * nk, 4), std::min(8, (budget - nk * BN * 128) / 16384));
     smem = (size_t)fixed + (size_t)stages * 16384 + (size_t)nk * BN * 128;
   } else {
-    const int stage_bytes = 16384 + BN * 128;
+    const int stage_bytes = (16384 + BN * 128) * (DT == FCM_F32 ? 2 : 1);
     stages = std::min(std::max(2 * nk, 4), std::min(8, budget / stage_bytes));
     if (stages < 2) return set_error(FCM_E_INFEASIBLE, "pw: not enough shared memory for 2 stages");
     smem = (size_t)fixed + (size_t)stages * stage_bytes;
@@ -1451,7 +1523,7 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
   while (ng > 1 && nbuf * ng * BN > 512) ng /= 2;
   auto kern = pw_tc_kernel<DT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_k(kern, dim3(grid), dim3(576), smem, st, ta, tb, ty, ep, M, N, K, BN, nbn, make_fdiv(nbn), stages, ng, nbuf,
+  launch_k(kern, dim3(grid), dim3(DT == FCM_F32 ? 640 : 576), smem, st, ta, tb, ty, ep, M, N, K, BN, nbn, make_fdiv(nbn), stages, ng, nbuf,
            pow2_cols(nbuf * ng * BN),
                                 ncap, resB ? 1 : 0, trace_buf(), debug_flags());
   const int rc = check_launch("pw_tc_kernel");
@@ -1462,6 +1534,7 @@ static int launch_pw_t(const void* x, const void* wp, const Epi& ep, void* y, in
 int launch_pw_tc(int dt, const void* x, const void* wp, const Epi& ep, void* y, int M, int K, int N, int nsplit,
                  cudaStream_t st) {
   switch (dt) {
+    case FCM_F32: return launch_pw_t<FCM_F32>(x, wp, ep, y, M, K, N, nsplit, st);
     case FCM_BF16: return launch_pw_t<FCM_BF16>(x, wp, ep, y, M, K, N, nsplit, st);
     case FCM_F16: return launch_pw_t<FCM_F16>(x, wp, ep, y, M, K, N, nsplit, st);
     case FCM_S8: return launch_pw_t<FCM_S8>(x, wp, ep, y, M, K, N, nsplit, st);

@@ -67,6 +67,11 @@ def test_pwdw_r_steady_state(fmt, s):
     Case("pwdw", fmt, n, h, h, c_in, c_mid, k=3, s=s, tile=tile).check()
 
 
+def test_pw_f32_3xtf32_steady_state():
+    # fp32 PW on the tensor cores (3xTF32): >= 3 tiles per CTA, 3 C_in chunks, 2 C_out slices
+    Case("pw", "f32", 4, 56, 56, 80, 192).check()
+
+
 @pytest.mark.parametrize("fmt", ["bf16", "f16"])
 def test_pwdw_r_wide_halo_steady_state(fmt):
     # 7 x 14 stride-2 output tiles (435 halo rows = 4 MMA row blocks), 32-byte X rows (C_in = 16)
