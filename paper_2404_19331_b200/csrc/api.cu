@@ -286,7 +286,11 @@ int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, con
   if (overlaps(x, y)) return set_error(FCM_E_INVAL, "dwpw: x and y overlap");
   Geo g{x->n, x->h, x->w, x->c, Ho, Wo, y->c, geom->k, geom->stride, geom->pad_t, geom->pad_l, 1, 0, 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (x->dtype == FCM_F32 || !pitch_ok(x) || !pitch_ok(y))
+  // fp32: the tensor-core kernel (DW on FFMA, PW 3xTF32) when its resident weight split fits shared
+  // memory, else the FFMA kernel (FCM_DWPW_F32_TC=0: always the FFMA kernel)
+  static const bool f32_tc = [] { const char* e = getenv("FCM_DWPW_F32_TC"); return !e || atoi(e) != 0; }();
+  const bool f32_try_tc = x->dtype == FCM_F32 && f32_tc && (geom->k == 3 || geom->k == 5);
+  if ((x->dtype == FCM_F32 && !f32_try_tc) || !pitch_ok(x) || !pitch_ok(y))
     return launch_dwpw_simt(x->dtype, x->data, w_dw, to_epi(ep_dw), w_pw_packed, to_epi(ep_pw), y->data, g, st);
   int nsplit = 0;
   default_dwpw_tile(g, dwpw_mmax(x->dtype, g), dwpw_pair_dt(x->dtype, g));
@@ -296,7 +300,12 @@ int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, con
     if (tile->tile_n > 0) g.nb = tile->tile_n;
     if (tile->n_split > 0) nsplit = tile->n_split;
   }
-  return launch_dwpw_tc(x->dtype, x->data, w_dw, to_epi(ep_dw), w_pw_packed, to_epi(ep_pw), y->data, g, nsplit, st);
+  const int rc = launch_dwpw_tc(x->dtype, x->data, w_dw, to_epi(ep_dw), w_pw_packed, to_epi(ep_pw), y->data, g, nsplit, st);
+  if (rc == FCM_E_INFEASIBLE && x->dtype == FCM_F32) {
+    Geo gs{x->n, x->h, x->w, x->c, Ho, Wo, y->c, geom->k, geom->stride, geom->pad_t, geom->pad_l, 1, 0, 0};
+    return launch_dwpw_simt(x->dtype, x->data, w_dw, to_epi(ep_dw), w_pw_packed, to_epi(ep_pw), y->data, gs, st);
+  }
+  return rc;
 }
 
 int fcm_pwpw(const fcm_tensor* x, const void* w1_packed, int32_t c_mid, const fcm_epilogue* ep1,

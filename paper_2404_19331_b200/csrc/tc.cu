@@ -593,11 +593,14 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
   uint8_t* smem = align1024(smem_raw);
   constexpr bool kPair = dwpw_pair<DT, K>();
   // A slot: pair core = no-swizzle K-major rows (MB x 128 rows, LBO = albo); else SW128, 128 rows
-  const int aslot = kPair ? ((8 * albo + 1023) & ~1023) : 16384;
+  // fp32 (3xTF32): the commBuffer holds T_hi and T_lo (the DW warps write both), the resident PW
+  // weights W and W_lo (split in place once per CTA by the DW warps)
+  constexpr bool kSplit = DT == FCM_F32;
+  const int aslot = kPair ? ((8 * albo + 1023) & ~1023) : (kSplit ? 32768 : 16384);
   uint8_t* abuf = smem;                          // na x aslot A operand (commBuffer) ring
   uint8_t* xbuf = abuf + na * aslot;             // XS x X halo chunks (TMA -> DW)
   uint8_t* bbuf = xbuf + XS * xstride;           // BS x PW weight chunks (TMA -> MMA); resB: BS = nk, loaded once
-  uint8_t* cst = bbuf + BS * BN * 128;
+  uint8_t* cst = bbuf + BS * BN * 128 * (kSplit ? 2 : 1);
   uint8_t* dcst = cst + consts_bytes<DT>(ncap);                 // DW epilogue constants [nk*KC]
   uint32_t* wsm = reinterpret_cast<uint32_t*>(dcst + consts_bytes<DT>(nk * KC));  // DW weights
   uint64_t* fullX = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(wsm) + dwpw_wbytes<DT, K>(nk));
@@ -608,7 +611,8 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
   uint64_t* aempty = afull + na;
   uint64_t* tfull = aempty + na;
   uint64_t* tempty = tfull + nacc;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + nacc);
+  uint64_t* bconv = tempty + nacc;               // kSplit: resident weights split
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bconv + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EpiS cs = stage_consts<DT>(ep, Cout, ncap, cst);
   const EpiS dcs = stage_consts<DT>(ed, Cin, nk * KC, dcst);
@@ -623,6 +627,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     for (int s = 0; s < BS; ++s) { mbar_init(fullB + s, 1); mbar_init(emptyB + s, 1); }
     for (int a = 0; a < na; ++a) { mbar_init(afull + a, kDwpwNDW); mbar_init(aempty + a, 1); }
     for (int a = 0; a < nacc; ++a) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4); }
+    mbar_init(bconv, kDwpwNDW);
     fence_barrier_init();
   }
   if (warp == WARP_MMA) tmem_alloc_rt(tslot, tmem_cols);
@@ -717,6 +722,7 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           cstamp(local * nk + kc, 6);
           if (kc == 0) stamp(local, 1);
           mbar_wait(fullB + sb, resB ? 0 : rb.ph);
+          if (kSplit && local == 0 && kc == 0) mbar_wait(bconv, 0);
           tc_fence_after();
           // kPair: A (the commBuffer) in the no-swizzle K-major layout, a K step = 2 chunks of albo,
           // row block h starts 128 rows (2 KB) further
@@ -735,11 +741,22 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
               adk[0][k] = ad + astep * k;
               adk[1][k] = ad + (2048 >> 4) + astep * k;
             }
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
+            if constexpr (kSplit) {  // T_hi.W_hi + T_hi.W_lo + T_lo.W_hi (MB == 1)
+              const uint64_t alo = 16384 >> 4, blo = (uint64_t)((nk * BN * 128) >> 4);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                if (h < MB && k < ksteps) mma_ss<KIND>(d + h * BN, adk[h][k], bdk[k], idesc, (kc | k) != 0);
+                if (k < ksteps) {
+                  mma_ss<KIND>(d, adk[0][k], bdk[k], idesc, (kc | k) != 0);
+                  mma_ss<KIND>(d, adk[0][k], bdk[k] + blo, idesc, 1);
+                  mma_ss<KIND>(d, adk[0][k] + alo, bdk[k], idesc, 1);
+                }
+            } else {
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  if (h < MB && k < ksteps) mma_ss<KIND>(d + h * BN, adk[h][k], bdk[k], idesc, (kc | k) != 0);
+            }
           }
           mma_commit(aempty + a);
           cstamp(local * nk + kc, 7);
@@ -771,6 +788,24 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     int kc_w = -1;
     Ring rx(XS), ra(na);
     int local = 0, phase = 0;
+    if constexpr (kSplit) {
+      // resident fp32 PW weights (the launcher requires resB): W -> W_hi in place, W_lo after the
+      // nk chunks (same SW128 positions), once per CTA; the MMA warp waits on bconv
+      for (int c = 0; c < nk; ++c) mbar_wait(fullB + c, 0);
+      const uint32_t b0 = smem_u32(bbuf), lo = (uint32_t)(nk * BN * 128);
+      for (int v = dw * 32 + lane; v < nk * BN * 8; v += kDwpwNDW * 32) {
+        const uint4 x = lds128(b0 + 16 * v);
+        const uint4 h = make_uint4(x.x & 0xFFFFE000u, x.y & 0xFFFFE000u, x.z & 0xFFFFE000u, x.w & 0xFFFFE000u);
+        sts128(b0 + 16 * v, h.x, h.y, h.z, h.w);
+        sts128(b0 + lo + 16 * v, __float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x)),
+               __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y)),
+               __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z)),
+               __float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w)));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bconv);
+    }
     // start of a C_in-chunk phase: X stage full and A slot free (relay barrier or own mbarrier waits)
     auto go = [&]() {
       if constexpr (FCM_DWPW_RELAY) {
@@ -931,7 +966,16 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
                                  [&](int yy, const typename Tr<DT>::acc_t(&acc)[V]) {
                                    const int m = (b * th + yy) * tw + x;
                                    const uint32_t word = (cl < Cin) ? epi_pack<DT>(acc, ec, ed) : 0u;
-                                   if (live) sts32(abase + sw128_off(m, wd), word);
+                                   if constexpr (kSplit) {  // T_hi (exact in tf32) and T_lo = T - T_hi
+                                     const uint32_t hi = word & 0xFFFFE000u;
+                                     if (live) {
+                                       sts32(abase + sw128_off(m, wd), hi);
+                                       sts32(abase + 16384 + sw128_off(m, wd),
+                                             __float_as_uint(__uint_as_float(word) - __uint_as_float(hi)));
+                                     }
+                                   } else {
+                                     if (live) sts32(abase + sw128_off(m, wd), word);
+                                   }
                                  });
           }
          }
@@ -999,6 +1043,26 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
             uint32_t r[16];
             tmem_ld16(tq + cb, r);
             tmem_ld_wait();
+            if constexpr (ES == 4) {  // fp32 output: act(acc * scale + bias) (+ residual), 4 x 16 B
+              if (ok) {
+                const float* rp = ep.residual ? static_cast<const float*>(ep.residual) + poh + cb : nullptr;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  if (cb + 4 * j < valid) {
+                    const uint4 sc = lds128(cs.base + 4 * (ns * BN + cb + 4 * j));
+                    const uint4 bi = lds128(cs.base + 4 * (cs.ncap + ns * BN + cb + 4 * j));
+                    uint4 rs = make_uint4(0u, 0u, 0u, 0u);
+                    if (rp) rs = ldg_nc128(rp + 4 * j);
+                    const float* a = reinterpret_cast<const float*>(&r[4 * j]);
+                    stg128(dst + cb * 4 + 16 * j,
+                           __float_as_uint(act_f(fmaf(a[0], __uint_as_float(sc.x), __uint_as_float(bi.x)), ep.act) + __uint_as_float(rs.x)),
+                           __float_as_uint(act_f(fmaf(a[1], __uint_as_float(sc.y), __uint_as_float(bi.y)), ep.act) + __uint_as_float(rs.y)),
+                           __float_as_uint(act_f(fmaf(a[2], __uint_as_float(sc.z), __uint_as_float(bi.z)), ep.act) + __uint_as_float(rs.z)),
+                           __float_as_uint(act_f(fmaf(a[3], __uint_as_float(sc.w), __uint_as_float(bi.w)), ep.act) + __uint_as_float(rs.w)));
+                  }
+              }
+              continue;
+            }
             uint32_t o[8];
             // (the residual: the shortcut input at the same NHWC position)
             epi16_any<DT, !R6>(r, cs, ep, ns * BN + cb, o, hasres, rcur.v[2 * hh], rcur.v[2 * hh + 1]);
@@ -1610,7 +1674,8 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   static const int na_env = [] { const char* e = getenv("FCM_NA"); return e ? atoi(e) : 0; }();  // dev override
   const int na = na_env ? na_env : kDwpwNA;
   const int nacc = 2;
-  const int aslot = kPair ? ((8 * albo + 1023) & ~1023) : 16384;
+  constexpr int kSp = DT == FCM_F32 ? 2 : 1;  // fp32 3xTF32: T_hi / T_lo slots, W / W_lo resident
+  const int aslot = kPair ? ((8 * albo + 1023) & ~1023) : 16384 * kSp;
   const int fixed = 1024 + na * aslot + consts_bytes<DT>(ncap) + consts_bytes<DT>(nk * KC) + dwpw_wbytes<DT, K>(nk) + 512;
   const int xstride = ((g.nb * th_in * tw_in * 128) + 1023) & ~1023;
   const int tiles_x = (g.Wo + g.tw - 1) / g.tw, tiles_y = (g.Ho + g.th - 1) / g.th;
@@ -1631,14 +1696,17 @@ static int launch_dwpw_t(const void* x, const void* wdw, const Epi& ed, const vo
   // phases wait on it), the weights are L2 hits either way
   static const int xs_min = [] { const char* e = getenv("FCM_XS_MIN"); return e ? atoi(e) : 4; }();
   const int resgrid = (grid / nsplit) * nsplit;
-  const int xs_res = std::min(xs_cap, (smem_cap - fixed - nk * BN * 128) / xstride);
-  const bool resB = nk <= 16 && resgrid > 0 && resgrid >= grid * 15 / 16 && xs_res >= 2 && xs_res >= std::min(XS, xs_min);
+  const int xs_res = std::min(xs_cap, (smem_cap - fixed - nk * BN * 128 * kSp) / xstride);
+  const bool resB = nk <= 16 && resgrid > 0 && resgrid >= grid * 15 / 16 && xs_res >= 2 &&
+                    (DT == FCM_F32 || xs_res >= std::min(XS, xs_min));
+  if (DT == FCM_F32 && !resB)  // the fp32 split keeps all weight chunks resident
+    return set_error(FCM_E_INFEASIBLE, "dwpw fp32 (3xTF32): the C_in x C_out slice does not fit shared memory");
   if (resB) {
     grid = resgrid;
     BS = nk;
     XS = xs_res;
   }
-  const size_t smem = (size_t)fixed + (size_t)BS * BN * 128 + (size_t)XS * xstride;
+  const size_t smem = (size_t)fixed + (size_t)BS * BN * 128 * (resB ? kSp : 1) + (size_t)XS * xstride;
   auto kern = dwpw_tc_kernel<DT, K, S>;
   if constexpr (dwpw_pair<DT, K>())
     if (ed.act == FCM_ACT_RELU6 && ep.act <= FCM_ACT_RELU6) kern = dwpw_tc_kernel<DT, K, S, true>;
@@ -1672,6 +1740,7 @@ static int launch_dwpw_dt(const void* x, const void* wdw, const Epi& ed, const v
 int launch_dwpw_tc(int dt, const void* x, const void* wdw, const Epi& ed, const void* wp, const Epi& ep, void* y,
                    const Geo& g, int ns, cudaStream_t st) {
   switch (dt) {
+    case FCM_F32: return launch_dwpw_dt<FCM_F32>(x, wdw, ed, wp, ep, y, g, ns, st);
     case FCM_BF16: return launch_dwpw_dt<FCM_BF16>(x, wdw, ed, wp, ep, y, g, ns, st);
     case FCM_F16: return launch_dwpw_dt<FCM_F16>(x, wdw, ed, wp, ep, y, g, ns, st);
     case FCM_S8: return launch_dwpw_dt<FCM_S8>(x, wdw, ed, wp, ep, y, g, ns, st);

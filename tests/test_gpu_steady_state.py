@@ -67,6 +67,12 @@ def test_pwdw_r_steady_state(fmt, s):
     Case("pwdw", fmt, n, h, h, c_in, c_mid, k=3, s=s, tile=tile).check()
 
 
+def test_dwpw_f32_3xtf32_steady_state():
+    # fp32 DWPW on the tensor-core kernel (T_hi / T_lo commBuffer, resident W / W_lo): >= 3 tiles
+    # per CTA, MobileNetV2 block-2 shape with its shortcut
+    Case("dwpw", "f32", 8, 56, 56, 144, 24, residual=True).check()
+
+
 def test_pw_f32_3xtf32_steady_state():
     # fp32 PW on the tensor cores (3xTF32): >= 3 tiles per CTA, 3 C_in chunks, 2 C_out slices
     Case("pw", "f32", 4, 56, 56, 80, 192).check()
