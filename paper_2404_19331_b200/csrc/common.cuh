@@ -709,6 +709,61 @@ __device__ __forceinline__ void dw3_cols_roll(uint32_t src, int row_bytes, int n
   }
 }
 
+// fp32 3x3 column-pair core (the fp32 DWPW's DW stage): a lane owns one fp32 channel of two
+// adjacent output columns; each tap is one packed fma.rn.f32x2 over (x[col0 tap], x[col1 tap]) with
+// the weight duplicated in both halves -- per column the same IEEE fp32 fma chain, in the same
+// (i, j) order, as the scalar core. Rolled 3-row window as in dw3_cols_roll. sink(r, c, acc).
+template <int S, int COLB, class Sink>
+__device__ __forceinline__ void dw3_pair_f32(uint32_t src, int row_bytes, int nrows, const uint64_t (&W2)[9],
+                                             Sink&& sink) {
+  constexpr int NCW = S + 3;  // input words of a row feeding the two output columns
+  auto load = [&](float (&dst)[NCW], int row) {
+    const uint32_t rp = src + row * row_bytes;
+#pragma unroll
+    for (int j = 0; j < NCW; ++j) dst[j] = __uint_as_float(lds32(rp + j * COLB));
+  };
+  auto out_row = [&](int r, const float (&x0)[NCW], const float (&x1)[NCW], const float (&x2)[NCW]) {
+    uint64_t acc = 0ull;  // (+0, +0)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) acc = f2_fma(f2_pack(x0[j], x0[S + j]), W2[j], acc);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) acc = f2_fma(f2_pack(x1[j], x1[S + j]), W2[3 + j], acc);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) acc = f2_fma(f2_pack(x2[j], x2[S + j]), W2[6 + j], acc);
+    float a, b;
+    f2_unpack(acc, a, b);
+    sink(r, 0, a);
+    sink(r, 1, b);
+  };
+  if constexpr (S == 1) {
+    float B0[NCW], B1[NCW], B2[NCW];
+    load(B0, 0);
+    load(B1, 1);
+    for (int r = 0; r < nrows; r += 3) {
+      load(B2, r + 2);
+      out_row(r, B0, B1, B2);
+      if (r + 1 >= nrows) break;
+      load(B0, r + 3);
+      out_row(r + 1, B1, B2, B0);
+      if (r + 2 >= nrows) break;
+      load(B1, r + 4);
+      out_row(r + 2, B2, B0, B1);
+    }
+  } else {
+    float E0[NCW], E1[NCW], O[NCW];
+    load(E0, 0);
+    for (int r = 0; r < nrows; r += 2) {
+      load(O, 2 * r + 1);
+      load(E1, 2 * r + 2);
+      out_row(r, E0, O, E1);
+      if (r + 1 >= nrows) break;
+      load(O, 2 * r + 3);
+      load(E0, 2 * r + 4);
+      out_row(r + 1, E1, O, E0);
+    }
+  }
+}
+
 // Activation dispatch: one instantiation per activation (the runtime value picks it once).
 template <class F>
 __device__ __forceinline__ void with_act(int act, F&& f) {

@@ -939,6 +939,47 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
           }
           }
          }
+         if constexpr (DT == FCM_F32 && K == 3) {
+          // fp32 3x3: column-pair FFMA2 core (a lane = one channel of two adjacent output columns),
+          // T written as T_hi / T_lo for the 3xTF32 PW; the same lane groups as the other cores
+          done = true;
+          const int cw_valid = min(32, Cin - kc * KC);
+          const int gs = cw_valid > 16 ? 32 : (cw_valid > 8 ? 16 : 8);
+          const int npix = 32 / gs, grp = lane / gs, wd = lane - grp * gs;
+          const int cl = kc * KC + wd;
+          uint64_t W2[9];
+          {
+            const uint32_t wa = smem_u32(wsm) + 4 * (kc * 32 + wd);
+#pragma unroll
+            for (int t9 = 0; t9 < 9; ++t9) {
+              const float w = __uint_as_float(lds32(wa + 4 * t9 * nk * 32));
+              W2[t9] = f2_pack(w, w);
+            }
+          }
+          const EpiC ec = epic<DT>(dcs, cl);
+          go();
+          const int ncolp = (tw + 1) >> 1;
+          const int ncg = (nb * ncolp + npix - 1) / npix;
+          for (int item = dw; item < ncg * nseg; item += kDwpwNDW) {
+            const int cg = item / nseg, seg = item - cg * nseg;
+            const int cpr = cg * npix + grp;
+            const bool live = cpr < nb * ncolp;
+            const int cpi = live ? cpr : cg * npix;
+            const int b = cpi / ncolp, x0 = 2 * (cpi - b * ncolp);
+            const int y0 = seg * kSeg;
+            const int nrows = live ? min(kSeg, th - y0) : 0;
+            const bool c1 = x0 + 1 < tw;
+            const uint32_t src = st + ((((b * th_in) + y0 * S) * tw_in + x0 * S) * 32 + wd) * 4;
+            dw3_pair_f32<S, 128>(src, tw_in * 128, nrows, W2, [&](int r, int c, float a) {
+              if (c == 1 && !c1) return;
+              const int m = (b * th + y0 + r) * tw + x0 + c;
+              const float v = cl < Cin ? act_f(fmaf(a, ec.sc, ec.bi), ed.act) : 0.f;
+              const uint32_t word = __float_as_uint(v), hi = word & 0xFFFFE000u;
+              sts32(abase + sw128_off(m, wd), hi);
+              sts32(abase + 16384 + sw128_off(m, wd), __float_as_uint(v - __uint_as_float(hi)));
+            });
+          }
+         }
          if (!done) {
           DwW<DT, K> W;
           // lane groups (as in the pair core): a partly filled channel chunk packs 2 or 4 output
