@@ -10,7 +10,7 @@ timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4 > $O/gputest.txt
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
 timeout 900 python bench.py --plan-out $O/plan_measured.json --layers-out $O/layers.json > $O/bench.json 2> $O/bench.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_reference.json 2> $O/bench_reference.err
-for cfg in "mobilenet_v1 s8 64" "mobilenet_v1 bf16 64" "efficientnet_b0 s8 256" "cvt13 bf16 512" "mobilenet_v2 bf16 1" "mobilenet_v2 bf16 64" "single_dwpw f32 1" "single_dwpw s8 1" "xception bf16 64" "xception s8 64" "proxylessnas_gpu bf16 64" "proxylessnas_gpu s8 64" "ceit_leff bf16 256" "cmt_irffn bf16 128" "cmt_irffn s8 128" "efficientnet_b0 bf16 256"; do
+for cfg in "mobilenet_v2 f32 64" "mobilenet_v1 s8 64" "mobilenet_v1 bf16 64" "efficientnet_b0 s8 256" "cvt13 bf16 512" "mobilenet_v2 bf16 1" "mobilenet_v2 bf16 64" "single_dwpw f32 1" "single_dwpw s8 1" "xception bf16 64" "xception s8 64" "proxylessnas_gpu bf16 64" "proxylessnas_gpu s8 64" "ceit_leff bf16 256" "cmt_irffn bf16 128" "cmt_irffn s8 128" "efficientnet_b0 bf16 256"; do
   set -- $cfg
   timeout 400 python bench.py --net $1 --dtype $2 --batch $3 --steps 50 --warmup 5 --no-cpu-baseline --plan-out $O/configs/plan_$1_$2_$3.json > $O/configs/bench_$1_$2_$3.json 2> $O/configs/bench_$1_$2_$3.err
 done
