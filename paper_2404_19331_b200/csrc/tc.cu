@@ -145,16 +145,20 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
             fminf(fmaxf(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]), lo_c), hi_c) + s.x,
             fminf(fmaxf(fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]), lo_c), hi_c) + s.y);
       }
-    } else if (e.act == FCM_ACT_NONE) {
-#pragma unroll
-      for (int w = 0; w < 8; ++w)
-        out[w] = pack2<DT, false>(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]),
-                                  fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]));
     } else {
+      // packed: one FFMA2 per column pair, cvt.rn(.relu) pack, min for RELU6 (bit-identical to the
+      // scalar fma / min / round: 6 is exact in bf16 / f16, rounding is monotonic)
+      auto pk = [&](auto actc) {
+        constexpr int ACT = decltype(actc)::value;
+        const uint32_t hc = ACT == FCM_ACT_RELU6 ? bound2<DT>(hi_c) : 0u;
 #pragma unroll
-      for (int w = 0; w < 8; ++w)
-        out[w] = pack2<DT, true>(fminf(fmaf(__uint_as_float(r[2 * w]), sc[2 * w], bi[2 * w]), hi_c),
-                                 fminf(fmaf(__uint_as_float(r[2 * w + 1]), sc[2 * w + 1], bi[2 * w + 1]), hi_c));
+        for (int w = 0; w < 8; ++w)
+          out[w] = epi_act2<DT, ACT>(__uint_as_float(r[2 * w]), __uint_as_float(r[2 * w + 1]),
+                                     f2_pack(sc[2 * w], sc[2 * w + 1]), f2_pack(bi[2 * w], bi[2 * w + 1]), hc);
+      };
+      if (e.act == FCM_ACT_NONE) pk(std::integral_constant<int, FCM_ACT_NONE>());
+      else if (e.act == FCM_ACT_RELU) pk(std::integral_constant<int, FCM_ACT_RELU>());
+      else pk(std::integral_constant<int, FCM_ACT_RELU6>());
     }
   }
 }
