@@ -136,8 +136,24 @@ __device__ __forceinline__ void epi16(const uint32_t* r, const EpiS& cs, const E
     }
     const float hi_c = act_hi(e.act);
     if constexpr (RES) {
-      const float lo_c = act_lo(e.act);
       const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+      if (e.act == FCM_ACT_NONE) {
+        // (the inverted-residual projection) packed: v = fma(acc, scale, bias) then + shortcut, two
+        // FFMA2 per column pair -- the same two roundings as the scalar form below
+        const uint64_t one2 = 0x3F8000003F800000ull;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const float2 sf = word2f<DT>(rw[w]);
+          const uint64_t v = f2_fma(f2_fma(f2_pack(__uint_as_float(r[2 * w]), __uint_as_float(r[2 * w + 1])),
+                                           f2_pack(sc[2 * w], sc[2 * w + 1]), f2_pack(bi[2 * w], bi[2 * w + 1])),
+                                    one2, f2_pack(sf.x, sf.y));
+          float v0, v1;
+          f2_unpack(v, v0, v1);
+          out[w] = pack2<DT, false>(v0, v1);
+        }
+        return;
+      }
+      const float lo_c = act_lo(e.act);
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
         const float2 s = word2f<DT>(rw[w]);
