@@ -568,6 +568,12 @@ __global__ void __launch_bounds__(DT == FCM_F32 ? 640 : 576, 1)
 #endif
 constexpr int kDwpwNC = FCM_DWPW_NC;
 template <int DT, int K> constexpr int dwpw_ndw() { return FCM_DWPW_NDW; }
+// relay waits: plain try_wait polling (FCM_RELAY_SLEEP=1: sleep back-off, development experiment)
+#if defined(FCM_RELAY_SLEEP) && FCM_RELAY_SLEEP
+#define RELAY_WAIT(b, p) mbar_wait_sleep<32>(b, p)
+#else
+#define RELAY_WAIT(b, p) mbar_wait(b, p)
+#endif
 constexpr int kDwpwNA = 2;  // default A-operand (commBuffer) ring depth
 struct DwDivs {
   FDiv hp;              // column pairs per image
@@ -791,9 +797,9 @@ __global__ void __launch_bounds__((4 + dwpw_ndw<DT, K>() + 4) * 32, 1)
     int p = 0;
     for (int t = blockIdx.x; t < total && FCM_DWPW_RELAY; t += gridDim.x)
       for (int kc = 0; kc < nk; ++kc, rx.next(), ra.next(), ++p) {
-        mbar_wait(fullX + rx.i, rx.ph);
+        RELAY_WAIT(fullX + rx.i, rx.ph);
         if (lane == 0) cstamp(p, 0);
-        mbar_wait(aempty + ra.i, ra.ph ^ 1);
+        RELAY_WAIT(aempty + ra.i, ra.ph ^ 1);
         if (lane == 0) cstamp(p, 1);
         named_bar_arrive(2 + (p & 1), kGoThreads);
       }
