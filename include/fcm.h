@@ -141,12 +141,17 @@ typedef struct {
 int fcm_dw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const fcm_epilogue* ep,
            fcm_tensor* y, const fcm_tile* tile, void* stream);
 
-/* Layer-by-layer pointwise conv. x [N,H,W,C_in], w_pw_packed from fcm_pack_pw, y [N,H,W,C_out]. */
+/* Layer-by-layer pointwise conv. x [N,H,W,C_in], w_pw_packed from fcm_pack_pw, y [N,H,W,C_out].
+ * bf16 / f16 / int8 on the tensor cores; fp32 too, as 3xTF32 (x_hi.w_hi + x_hi.w_lo + x_lo.w_hi,
+ * ~fp32 accuracy; env FCM_PW_F32_TC=0 selects the FFMA kernel). Pixel pitches that are not a
+ * multiple of 16 B run the CUDA-core kernel. */
 int fcm_pw(const fcm_tensor* x, const void* w_pw_packed, const fcm_epilogue* ep, fcm_tensor* y,
            const fcm_tile* tile, void* stream);
 
 /* FCM DWPW: y = PW(DW(x)). x [N,H,W,C_in], w_dw [k][k][C_in], w_pw_packed (C_in -> C_out),
- * y [N,Ho,Wo,C_out]. For int8, ep_pw->zp_in must equal ep_dw->zp_out (T's zero point). */
+ * y [N,Ho,Wo,C_out]. For int8, ep_pw->zp_in must equal ep_dw->zp_out (T's zero point). fp32 runs the
+ * tensor-core kernel (3xTF32 PW) when the C_in x C_out weights and their split fit shared memory,
+ * else the FFMA kernel. */
 int fcm_dwpw(const fcm_tensor* x, const void* w_dw, const fcm_dw_geom* geom, const fcm_epilogue* ep_dw,
              const void* w_pw_packed, const fcm_epilogue* ep_pw, fcm_tensor* y, const fcm_tile* tile,
              void* stream);
