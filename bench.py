@@ -132,8 +132,8 @@ def kernel_family(op, dtype=None, layer=None):
         wo = (layer["w"] + 2 * (k // 2) - k) // s + 1
         if s == 1 and k in (3, 5) and c % 16 == 0 and ho >= 14 and wo >= 14 and (k == 3 or c <= 512):
             return "dw_tc_i8_kernel"
-    if dtype == "f32" and op in ("dwpw", "pwdw_r"):  # the fused fp32 FCMs run on FFMA
-        return {"dwpw": "dwpw_simt_kernel", "pwdw_r": "pwdw_simt_kernel"}[op]
+    if dtype == "f32" and op == "pwdw_r":  # fp32 PWDW_R runs on FFMA (fp32 DWPW: the tensor-core kernel
+        return "pwdw_simt_kernel"          # when its weight split fits shared memory)
     return {"dw": "dw_nhwc_kernel", "pw": "pw_tc_kernel", "dwpw": "dwpw_tc_kernel", "pwdw_r": "pwdw_tc_kernel",
             "pwpw": "pwpw_tc_kernel"}[op]
 
